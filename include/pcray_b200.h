@@ -1,0 +1,296 @@
+/*
+ * pcray_b200.h — C ABI of the B200-native point-cloud ray launcher
+ * (arXiv 2402.13747: voxelization -> coarse path tracing -> path refinement).
+ *
+ * This is the drop-in boundary. The reference (`pcray`, /root/reference/proj)
+ * exposes its hot path as the static C++ API in proj/include/pcray/*.hpp; each
+ * entry point below replaces one of those functions (cited per function) and
+ * keeps its argument meaning, output order and error strings. Everything crosses
+ * as plain pointers and sizes: no C++ or torch types appear here.
+ *
+ * Conventions
+ *   - 3-vectors are 3 consecutive doubles (x, y, z); arrays of them are n*3.
+ *   - Every function returns 0 (PCR_OK) or a nonzero pcr_status; the message is
+ *     then available from pcr_last_error(ctx). Messages reproduce the reference's
+ *     std::runtime_error texts ("grid too large", "empty scene", "voxel_size must
+ *     be > 0", "division_factor must be >= 1", stage prefixes "validate: " ...).
+ *   - Result structs are allocated by the library and released with the matching
+ *     pcr_free_* call. Input buffers are caller-owned and only read.
+ *   - One context per device; calls on one context are serialised internally.
+ *
+ * The oracle wrapper (oracle/ref_capi.cpp, test infrastructure) fills the same
+ * result structs from the unmodified reference so tests compare field by field.
+ */
+#ifndef PCRAY_B200_H
+#define PCRAY_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCR_ABI_VERSION 1
+
+typedef enum pcr_status {
+  PCR_OK = 0,
+  PCR_ERR_INVALID = 1,  /* bad argument / precondition (reference: std::runtime_error) */
+  PCR_ERR_CUDA = 2,     /* CUDA runtime failure, message "… cuda <name>: <string>" */
+  PCR_ERR_NOMEM = 3,    /* device or host allocation failure */
+  PCR_ERR_RUNTIME = 4   /* any other failure; message carries the reference text */
+} pcr_status;
+
+/* IeKind (proj/include/pcray/voxel_grid.hpp:19) */
+enum { PCR_IE_SURFACE = 0, PCR_IE_EDGE = 1, PCR_IE_RECEIVER = 2 };
+/* InteractionKind (proj/include/pcray/tracer.hpp:29) */
+enum { PCR_REFLECTION = 0, PCR_DIFFRACTION = 1 };
+/* RejectReason (proj/include/pcray/refine.hpp:17) */
+enum { PCR_RAY_MISSED = 0, PCR_NOT_CONVERGED = 1, PCR_OCCLUDED = 2, PCR_DEGENERATE = 3 };
+
+#define PCR_MARCH_NO_IES 2147483647 /* kMarchNoIes, voxel_grid.hpp:22 */
+#define PCR_NO_IE 0xffffffffu       /* kNoIe, tracer.hpp:14 */
+
+/* Scene (proj/include/pcray/scene.hpp:11-46), flattened. */
+typedef struct pcr_scene_desc {
+  const double* point_position; /* n_points*3 */
+  const double* point_normal;   /* n_points*3 */
+  const uint32_t* point_label;  /* n_points   */
+  uint64_t n_points;
+  const double* edge_geometry;  /* n_edges*12: start, end, normal_a, normal_b */
+  const uint32_t* edge_label;   /* n_edges */
+  uint32_t n_edges;
+  const double* tx_position;    /* n_tx*3 */
+  const uint32_t* tx_id;        /* n_tx   */
+  uint32_t n_tx;
+  const double* rx_position;    /* n_rx*3 */
+  const uint32_t* rx_id;        /* n_rx   */
+  uint32_t n_rx;
+  double carrier_frequency_hz;
+} pcr_scene_desc;
+
+/* VoxelizationParams (voxel_grid.hpp:13-17) */
+typedef struct pcr_voxel_params {
+  double voxel_size;
+  int32_t division_factor;
+  uint64_t max_cells;
+} pcr_voxel_params;
+
+/* TraceParams (tracer.hpp:16-22); cone_apex_angle in radians. */
+typedef struct pcr_trace_params {
+  int32_t max_interactions;
+  int32_t kappa;
+  double cone_apex_angle;
+  int32_t diffraction_ray_count;
+  int32_t max_diffractions;
+} pcr_trace_params;
+
+/* RefineParams (refine.hpp:10-15) */
+typedef struct pcr_refine_params {
+  double delta;
+  int32_t rho;
+  double step_size;
+  int32_t fresnel_enabled;
+} pcr_refine_params;
+
+/* RunConfig physics and control fields (pipeline.hpp:12-32); file paths and
+ * radio lists are not part of run_pipeline_on_scene's contract. */
+typedef struct pcr_run_config {
+  double carrier_frequency_hz;
+  double voxel_size_m;
+  int32_t division_factor;
+  int32_t kappa;
+  int32_t max_interactions;
+  int32_t max_diffractions;
+  double cone_apex_angle_deg;
+  int32_t diffraction_ray_count;
+  double delta;
+  int32_t rho;
+  double step_size;
+  uint32_t seed;
+  int32_t thread_count; /* host hint only; never a correctness factor */
+  int32_t fresnel_enabled;
+} pcr_run_config;
+
+/* Host mirror of VoxelGrid (voxel_grid.hpp:58-94); IE fields as SoA. */
+typedef struct pcr_grid_host {
+  double origin[3];
+  int32_t dims[3];
+  double voxel_size;
+  int32_t division_factor;
+  uint64_t n_cells, n_ies, n_point_indices;
+  uint32_t* cell_ie_begin;    /* n_cells */
+  uint32_t* cell_ie_end;      /* n_cells */
+  int32_t* cell_march;        /* n_cells */
+  uint8_t* ie_kind;           /* n_ies */
+  uint32_t* ie_label;
+  double* ie_reception_point; /* n_ies*3 */
+  double* ie_sphere_center;   /* n_ies*3 */
+  double* ie_sphere_radius;   /* n_ies   */
+  uint32_t* ie_point_begin;
+  uint32_t* ie_point_end;
+  double* ie_seg_start;       /* n_ies*3 */
+  double* ie_seg_end;         /* n_ies*3 */
+  uint32_t* ie_edge_index;
+  uint32_t* ie_rx_id;
+  uint8_t* ie_planar;
+  double* ie_plane_point;     /* n_ies*3 */
+  double* ie_plane_normal;    /* n_ies*3 */
+  uint32_t* ie_voxel;
+  uint32_t* ie_subvoxel;
+  uint32_t* point_indices;    /* n_point_indices */
+} pcr_grid_host;
+
+/* A list of paths: PathCandidate (tracer.hpp:49-56) or ExactPath
+ * (refine.hpp:52-62). Interaction arrays are row-major [n][stride]. */
+typedef struct pcr_paths {
+  uint64_t n;
+  uint32_t stride;
+  uint32_t* tx_id;
+  uint32_t* rx_id;
+  double* tx_position;   /* n*3 */
+  double* rx_position;   /* n*3 */
+  double* length;        /* coarse_length (candidates) or total_length (exact) */
+  double* delay;         /* exact only */
+  uint8_t* converged;    /* exact only */
+  double* gradient_norm; /* exact only */
+  uint32_t* n_inter;     /* n */
+  uint8_t* kind;         /* n*stride */
+  double* position;      /* n*stride*3 */
+  uint32_t* label;       /* n*stride */
+  double* normal;        /* n*stride*3 */
+  uint32_t* ie_index;    /* n*stride */
+  uint32_t* edge_index;  /* n*stride */
+} pcr_paths;
+
+/* InitialHit list (tracer.hpp:58-64) */
+typedef struct pcr_initial_hits {
+  uint64_t n;
+  uint32_t* ie_index;
+  uint8_t* kind;
+  double* position; /* n*3 */
+  double* normal;   /* n*3 */
+  double* incoming; /* n*3 */
+} pcr_initial_hits;
+
+/* RefineOutcome per candidate (refine.hpp:64-67) */
+typedef struct pcr_outcomes {
+  pcr_paths paths;  /* row i valid iff has_path[i] */
+  uint8_t* has_path;
+  int32_t* reason;
+} pcr_outcomes;
+
+#define PCR_MAX_STAGES 16
+/* RunSummary (pipeline.hpp:46-58) plus device work counters. */
+typedef struct pcr_summary {
+  uint64_t point_count, edge_count, ie_count;
+  int32_t grid_dims[3];
+  uint64_t coarse_paths, refined_paths, rejected[4], exact_paths;
+  uint32_t n_timings;
+  char timing_stage[PCR_MAX_STAGES][16];
+  double timing_seconds[PCR_MAX_STAGES];
+  uint64_t hash;
+  pcr_paths paths;
+  /* work counters (product library only; zero from the oracle) */
+  uint64_t transmission_rays; /* sum over TX of n_IE */
+  uint64_t cone_traces;       /* voxel_cone_trace invocations (= dfs_trace calls) */
+  uint64_t visibility_tests;  /* segment_visible invocations */
+  uint64_t refine_iterations; /* refinement iterations summed over candidates */
+} pcr_summary;
+
+/* A conical ray (tracer.hpp:40-47) for the batch primitives; planes are given
+ * as (point, normal) pairs, provenance as the origin IE and label only. */
+typedef struct pcr_ray_desc {
+  double origin[3];
+  double direction[3];
+  double apex_angle;
+  int32_t n_planes; /* 0..2 */
+  double plane_point[2][3];
+  double plane_normal[2][3];
+  uint32_t origin_ie;    /* provenance.back().ie_index or PCR_NO_IE */
+  uint32_t origin_label; /* provenance.back().label */
+} pcr_ray_desc;
+
+/* Receptions of one batch of cone traces (tracer.hpp:71-76), CSR by ray. */
+typedef struct pcr_receptions {
+  uint64_t n_rays, n;
+  uint64_t* ray_offset; /* n_rays+1 */
+  uint32_t* ie_index;   /* n, ascending within a ray */
+  double* reception_point; /* n*3 */
+  uint8_t* hit_valid;
+  double* hit_position; /* n*3 */
+  double* hit_normal;   /* n*3 */
+  uint32_t* hit_label;
+  double* hit_distance;
+  uint64_t* evaluated_offset; /* n_rays+1 (debug: TraceDebug::evaluated, order-free) */
+  uint32_t* evaluated;        /* cell indices */
+} pcr_receptions;
+
+typedef struct pcr_ctx pcr_ctx;
+typedef struct pcr_scene pcr_scene; /* device-resident scene */
+typedef struct pcr_grid pcr_grid;   /* device-resident VoxelGrid */
+
+/* ---- context ------------------------------------------------------------ */
+int pcr_abi_version(void);
+int pcr_create(int device, pcr_ctx** out);
+void pcr_destroy(pcr_ctx* ctx);
+const char* pcr_last_error(const pcr_ctx* ctx);
+/* number of library kernel launches issued by this process (bench accounting) */
+uint64_t pcr_kernel_launches(void);
+
+/* ---- scene / grid residency ----------------------------------------------- */
+int pcr_scene_upload(pcr_ctx* ctx, const pcr_scene_desc* desc, pcr_scene** out);
+void pcr_scene_free(pcr_scene* scene);
+/* build_grid (voxel_grid.hpp:99; voxel_grid.cpp:82-227), device-resident result */
+int pcr_build_grid(pcr_ctx* ctx, const pcr_scene* scene, const pcr_voxel_params* params,
+                   pcr_grid** out);
+/* hand-built grids (tests build VoxelGrid by hand: test_voxel_grid.cpp:216-233) */
+int pcr_grid_upload(pcr_ctx* ctx, const pcr_grid_host* host, pcr_grid** out);
+/* compute_march_distances (voxel_grid.hpp:103; voxel_grid.cpp:229-268), in place */
+int pcr_compute_march_distances(pcr_ctx* ctx, pcr_grid* grid);
+int pcr_grid_download(pcr_ctx* ctx, const pcr_grid* grid, pcr_grid_host** out);
+void pcr_grid_free(pcr_grid* grid);
+void pcr_free_grid_host(pcr_grid_host* host);
+
+/* ---- stage 2: coarse tracing ---------------------------------------------- */
+/* transmission_phase (tracer.hpp:94-95; tracer.cpp:207-255) for TX number tx_index */
+int pcr_transmission_phase(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene,
+                           uint32_t tx_index, const pcr_trace_params* params,
+                           pcr_paths** los_out, pcr_initial_hits** hits_out);
+/* propagate (tracer.hpp:122-124; tracer.cpp:476-533); hits may be any list */
+int pcr_propagate(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene, uint32_t tx_index,
+                  const pcr_initial_hits* hits, const pcr_trace_params* params,
+                  pcr_paths** out);
+/* voxel_cone_trace (tracer.hpp:118-120; tracer.cpp:313-403) over a batch of rays */
+int pcr_cone_trace_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene,
+                         const pcr_ray_desc* rays, uint64_t n_rays, int want_debug,
+                         pcr_receptions** out);
+/* segment_visible (tracer.hpp:88-89; tracer.cpp:138-205) over a batch */
+int pcr_segment_visible_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene,
+                              const double* origin, const double* target,
+                              const uint32_t* target_ie, uint64_t n, uint8_t* visible_out);
+
+/* ---- stage 3: refinement ---------------------------------------------------- */
+/* refine_path (refine.hpp:77-78; refine.cpp:189-286) over a candidate list */
+int pcr_refine_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene,
+                     const pcr_paths* candidates, const pcr_refine_params* params,
+                     pcr_outcomes** out);
+
+/* ---- whole pipeline --------------------------------------------------------- */
+/* run_pipeline_on_scene (pipeline.hpp:61; pipeline.cpp:99-212) */
+int pcr_run_pipeline_on_scene(pcr_ctx* ctx, const pcr_scene_desc* scene,
+                              const pcr_run_config* config, pcr_summary** out);
+/* config_hash (pipeline.hpp:39; pipeline.cpp:89-97) */
+uint64_t pcr_config_hash(const pcr_run_config* config);
+void pcr_run_config_defaults(pcr_run_config* config);
+
+void pcr_free_paths(pcr_paths* p);
+void pcr_free_initial_hits(pcr_initial_hits* h);
+void pcr_free_outcomes(pcr_outcomes* o);
+void pcr_free_summary(pcr_summary* s);
+void pcr_free_receptions(pcr_receptions* r);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCRAY_B200_H */

@@ -1,0 +1,104 @@
+// common.cuh — error mapping, stream-ordered device buffers and launch helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+namespace pcr {
+
+// Errors surface through the C ABI as pcr_last_error(); messages reproduce the
+// reference's std::runtime_error texts where one exists.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define PCR_CUDA(call)                                                                          \
+  do {                                                                                          \
+    cudaError_t pcr_e_ = (call);                                                                \
+    if (pcr_e_ != cudaSuccess) {                                                                \
+      throw ::pcr::Error(pcr_e_ == cudaErrorMemoryAllocation ? 3 : 2,                           \
+                         std::string("cuda ") + #call + ": " + cudaGetErrorString(pcr_e_));    \
+    }                                                                                           \
+  } while (0)
+
+#define PCR_LAUNCH_CHECK() PCR_CUDA(cudaGetLastError())
+
+// Stream-ordered device buffer (cudaMallocAsync pool); never copied, only moved.
+template <typename T>
+class DBuf {
+ public:
+  DBuf() = default;
+  DBuf(size_t n, cudaStream_t s) { alloc(n, s); }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept { swap(o); }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      swap(o);
+    }
+    return *this;
+  }
+  void alloc(size_t n, cudaStream_t s) {
+    release();
+    stream_ = s;
+    n_ = n;
+    if (n) PCR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+  }
+  // Grow to at least n elements, keeping the first `keep` elements.
+  void reserve(size_t n, size_t keep, cudaStream_t s) {
+    if (n <= n_) return;
+    T* q = nullptr;
+    PCR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&q), n * sizeof(T), s));
+    if (keep && p_) PCR_CUDA(cudaMemcpyAsync(q, p_, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    if (p_) cudaFreeAsync(p_, stream_);
+    p_ = q;
+    n_ = n;
+    stream_ = s;
+  }
+  void release() {
+    if (p_) cudaFreeAsync(p_, stream_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+  void swap(DBuf& o) noexcept {
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+    std::swap(stream_, o.stream_);
+  }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+  cudaStream_t stream_ = nullptr;
+};
+
+inline unsigned blocks_for(uint64_t n, unsigned threads, unsigned cap = 148u * 64u) {
+  uint64_t b = (n + threads - 1) / threads;
+  if (b == 0) b = 1;
+  return static_cast<unsigned>(b < cap ? b : cap);
+}
+
+template <typename T>
+void d2h(T* dst, const T* src, size_t n, cudaStream_t s) {
+  if (n) PCR_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+}
+template <typename T>
+void h2d(T* dst, const T* src, size_t n, cudaStream_t s) {
+  if (n) PCR_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+// Launch accounting: every kernel launch of the library goes through this
+// counter so bench.py can report how many of our kernels ran in a timed region.
+extern uint64_t g_launch_count;
+inline void count_launch() { ++g_launch_count; }
+
+}  // namespace pcr

@@ -1,0 +1,135 @@
+// device_state.cuh — owning device containers behind the C-ABI handles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "geom.cuh"
+
+namespace pcr {
+
+// Device-resident scene (pcr_scene). Edges and radios are also kept on the host:
+// they are tiny and the bounds / radio bookkeeping reads them there.
+struct SceneDev {
+  uint64_t n_points = 0;
+  DBuf<double> pos, nrm;  // n*3
+  DBuf<uint32_t> label;
+  uint32_t n_edges = 0;
+  DBuf<double> edges;  // n_edges*12
+  DBuf<uint32_t> edge_label;
+  std::vector<double> h_edges;
+  std::vector<uint32_t> h_edge_label;
+  std::vector<double> h_tx, h_rx;  // n*3
+  std::vector<uint32_t> h_tx_id, h_rx_id;
+  DBuf<double> rx_pos;  // n_rx*3
+  DBuf<uint32_t> rx_id;
+  double carrier_frequency_hz = 60e9;
+
+  SceneView view() const {
+    SceneView v;
+    v.pos = pos.get();
+    v.nrm = nrm.get();
+    v.label = label.get();
+    v.n_points = n_points;
+    v.edges = edges.get();
+    v.edge_label = edge_label.get();
+    v.n_edges = n_edges;
+    return v;
+  }
+};
+
+// Device-resident VoxelGrid (pcr_grid).
+struct GridDev {
+  V3 origin{0, 0, 0};
+  int dims[3] = {0, 0, 0};
+  double voxel_size = 0.5;
+  int dv = 2;
+  double sub_edge = 0, sub_radius = 0, voxel_radius = 0, hit_eps = 0;
+  uint64_t n_cells = 0, n_ies = 0, n_pidx = 0;
+  DBuf<int4> cells;
+  DBuf<uint32_t> meta, label, edge, rx, voxel, sub, pidx;
+  DBuf<double4> sc, rp, pp, pn, seg_s, seg_e;
+  DBuf<uint2> range;
+
+  void set_geometry(const V3& o, const int d[3], double vs, int dvv) {
+    origin = o;
+    dims[0] = d[0];
+    dims[1] = d[1];
+    dims[2] = d[2];
+    voxel_size = vs;
+    dv = dvv;
+    // voxel_grid.hpp:68-71
+    sub_edge = voxel_size / dv;
+    sub_radius = 0.5 * std::sqrt(3.0) * sub_edge;
+    voxel_radius = 0.5 * std::sqrt(3.0) * voxel_size;
+    hit_eps = 1e-4 * voxel_size;
+  }
+
+  GridView view() const {
+    GridView v;
+    v.origin = origin;
+    v.dims[0] = dims[0];
+    v.dims[1] = dims[1];
+    v.dims[2] = dims[2];
+    v.voxel_size = voxel_size;
+    v.dv = dv;
+    v.sub_edge = sub_edge;
+    v.sub_radius = sub_radius;
+    v.voxel_radius = voxel_radius;
+    v.hit_eps = hit_eps;
+    v.n_cells = static_cast<uint32_t>(n_cells);
+    v.n_ies = static_cast<uint32_t>(n_ies);
+    v.cells = cells.get();
+    v.ie_meta = meta.get();
+    v.ie_label = label.get();
+    v.ie_sc = sc.get();
+    v.ie_rp = rp.get();
+    v.ie_pp = pp.get();
+    v.ie_pn = pn.get();
+    v.ie_range = range.get();
+    v.ie_edge = edge.get();
+    v.ie_rx = rx.get();
+    v.point_indices = pidx.get();
+    return v;
+  }
+  void alloc_ies(uint64_t n, cudaStream_t s) {
+    n_ies = n;
+    const size_t m = n ? n : 1;
+    meta.alloc(m, s);
+    label.alloc(m, s);
+    edge.alloc(m, s);
+    rx.alloc(m, s);
+    voxel.alloc(m, s);
+    sub.alloc(m, s);
+    sc.alloc(m, s);
+    rp.alloc(m, s);
+    pp.alloc(m, s);
+    pn.alloc(m, s);
+    seg_s.alloc(m, s);
+    seg_e.alloc(m, s);
+    range.alloc(m, s);
+  }
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  std::mutex mu;
+  // sin/cos table of the Keller fan azimuths, keyed by ray count (tracer.cpp:288-301)
+  int fan_n = 0;
+  DBuf<double> fan_table;  // n*6: cos phi, sin phi, sin(phi+dphi/2), cos(phi+dphi/2), sin(phi-dphi/2), cos(phi-dphi/2)
+  int sm_count = 148;
+};
+
+// stage 1 (voxelize.cu)
+void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int division_factor,
+                       uint64_t max_cells, GridDev& out);
+void compute_march_distances_device(Ctx& ctx, GridDev& grid);
+
+}  // namespace pcr

@@ -1,0 +1,382 @@
+// geom.cuh — device views of the scene and the voxel grid, and the per-ray
+// primitives every stage shares: point-set intersection (surface.cpp), the
+// Amanatides–Woo walker, cone/sphere tests and straight-line visibility
+// (tracer.cpp). Each function follows the cited reference lines operation by
+// operation (see exact.cuh for the arithmetic-order contract).
+#pragma once
+
+#include <cstdint>
+
+#include "exact.cuh"
+
+namespace pcr {
+
+enum : uint32_t { kSurface = 0, kEdge = 1, kReceiver = 2 };
+constexpr uint32_t kNoIe = 0xffffffffu;
+constexpr int32_t kMarchNoIes = 2147483647;
+
+// Device-resident VoxelGrid (voxel_grid.hpp:58-94). IE fields are SoA; the four
+// vectors used by the hot loops are padded to double4 so one record is two
+// 16-byte loads. sc.w carries sphere_radius.
+struct GridView {
+  V3 origin;
+  int dims[3];
+  double voxel_size;
+  int dv;
+  double sub_edge, sub_radius, voxel_radius, hit_eps;  // grid helpers, host-computed (voxel_grid.hpp:68-71)
+  uint32_t n_cells, n_ies;
+  const int4* cells;          // {ie_begin, ie_end, march, 0}
+  const uint32_t* ie_meta;    // bits 0-1: kind, bit 2: planar
+  const uint32_t* ie_label;
+  const double4* ie_sc;       // sphere center, w = sphere radius
+  const double4* ie_rp;       // reception point
+  const double4* ie_pp;       // plane point
+  const double4* ie_pn;       // plane normal
+  const uint2* ie_range;      // point_begin, point_end
+  const uint32_t* ie_edge;
+  const uint32_t* ie_rx;
+  const uint32_t* point_indices;
+};
+
+// Device-resident Scene (scene.hpp:38-46).
+struct SceneView {
+  const double* pos;  // n*3
+  const double* nrm;  // n*3
+  const uint32_t* label;
+  uint64_t n_points;
+  const double* edges;  // n_edges*12
+  const uint32_t* edge_label;
+  uint32_t n_edges;
+};
+
+__device__ __forceinline__ V3 ld3(const double4& v) { return V3{v.x, v.y, v.z}; }
+__device__ __forceinline__ V3 ie_center(const GridView& g, uint32_t i) { return ld3(g.ie_sc[i]); }
+__device__ __forceinline__ double ie_radius(const GridView& g, uint32_t i) { return g.ie_sc[i].w; }
+__device__ __forceinline__ uint32_t ie_kind(const GridView& g, uint32_t i) { return g.ie_meta[i] & 3u; }
+__device__ __forceinline__ bool ie_planar(const GridView& g, uint32_t i) { return (g.ie_meta[i] >> 2) & 1u; }
+
+__device__ __forceinline__ bool in_bounds(const GridView& g, int x, int y, int z) {
+  return x >= 0 && y >= 0 && z >= 0 && x < g.dims[0] && y < g.dims[1] && z < g.dims[2];
+}
+__device__ __forceinline__ uint32_t linear_index(const GridView& g, int x, int y, int z) {
+  return static_cast<uint32_t>(x + g.dims[0] * (y + g.dims[1] * z));
+}
+// voxel_grid.hpp:90-92: origin + (v + 0.5) * voxel_size
+__device__ __forceinline__ V3 voxel_center(const GridView& g, int x, int y, int z) {
+  return V3{g.origin.x + (static_cast<double>(x) + 0.5) * g.voxel_size,
+            g.origin.y + (static_cast<double>(y) + 0.5) * g.voxel_size,
+            g.origin.z + (static_cast<double>(z) + 0.5) * g.voxel_size};
+}
+
+// ---------------------------------------------------------------------------------
+// Point-set intersection (surface.cpp)
+struct SurfaceHit {
+  V3 position, normal;
+  uint32_t label;
+  double distance;
+};
+
+struct SurfaceEstimate {
+  V3 p_bar, n_bar;
+  double sdf, weight_sum;
+};
+
+// estimate_surface (surface.cpp:24-62). Non-planar payloads only; exp() is CUDA's
+// (<= 1 ulp from glibc's).
+__device__ inline SurfaceEstimate estimate_surface(const V3& x, uint32_t ie, const GridView& g,
+                                                   const SceneView& s) {
+  const double h = g.sub_edge;
+  const double inv_h2 = 1.0 / (h * h);
+  V3 p_sum{0, 0, 0}, n_sum{0, 0, 0};
+  double w_sum = 0.0;
+  double best_d2 = 1.7976931348623157e308;
+  const uint2 r = g.ie_range[ie];
+  uint32_t best = r.x;
+  for (uint32_t i = r.x; i < r.y; ++i) {
+    const uint32_t pi = g.point_indices[i];
+    const V3 p = load3(s.pos + 3ull * pi);
+    const V3 n = load3(s.nrm + 3ull * pi);
+    const double d2 = sqnorm(x - p);
+    if (d2 < best_d2) {
+      best_d2 = d2;
+      best = i;
+    }
+    const double w = exp(-d2 * inv_h2);
+    w_sum += w;
+    p_sum = p_sum + w * p;
+    n_sum = n_sum + w * n;
+  }
+  SurfaceEstimate est;
+  if (w_sum > 0.0 && norm(n_sum) > 0.0) {
+    est.p_bar = p_sum / w_sum;
+    est.n_bar = normalized(n_sum);
+    est.weight_sum = w_sum;
+  } else {
+    const uint32_t pi = g.point_indices[best];
+    est.p_bar = load3(s.pos + 3ull * pi);
+    est.n_bar = load3(s.nrm + 3ull * pi);
+    est.weight_sum = 0.0;
+  }
+  est.sdf = dot(x - est.p_bar, est.n_bar);
+  return est;
+}
+
+// sdf_value_at (surface.cpp:16-20)
+__device__ __forceinline__ double sdf_value_at(const V3& x, uint32_t ie, bool planar, const V3& pp,
+                                               const V3& pn, const GridView& g, const SceneView& s) {
+  if (planar) return dot(x - pp, pn);
+  return estimate_surface(x, ie, g, s).sdf;
+}
+
+// march_segment (surface.cpp:64-134); returns false for std::nullopt.
+__device__ inline bool march_segment(const V3& origin, const V3& dir, uint32_t ie, const GridView& g,
+                                     const SceneView& s, double t_max, SurfaceHit* out) {
+  const double eps = g.hit_eps;
+  const double4 sc4 = g.ie_sc[ie];
+  const V3 sc = ld3(sc4);
+  const double r = sc4.w;
+  const double t_center = dot(sc - origin, dir);
+  const double t_lo = smax(0.0, t_center - r);
+  const double t_hi = smin(t_center + r, t_max);
+  if (t_hi <= t_lo) return false;
+
+  const bool planar = ie_planar(g, ie);
+  V3 pp{0, 0, 0}, pn{0, 0, 1};
+  if (planar) {
+    pp = ld3(g.ie_pp[ie]);
+    pn = ld3(g.ie_pn[ie]);
+  }
+  auto make_hit = [&](double t) {
+    if (planar) {
+      const double dn = dot(dir, pn);
+      if (fabs(dn) > 1e-12) {
+        const double t_star = dot(pp - origin, pn) / dn;
+        if (t_star >= t_lo && t_star <= t_hi) t = t_star;
+      }
+    }
+    const V3 pos = origin + t * dir;
+    if (out) {
+      out->position = pos;
+      out->normal = planar ? pn : estimate_surface(pos, ie, g, s).n_bar;
+      out->label = g.ie_label[ie];
+      out->distance = t;
+    }
+    return true;
+  };
+
+  double t = t_lo;
+  double f = sdf_value_at(origin + t * dir, ie, planar, pp, pn, g, s);
+  if (fabs(f) <= eps) return make_hit(t);
+
+  if (planar) {
+    const double f_hi = sdf_value_at(origin + t_hi * dir, ie, planar, pp, pn, g, s);
+    if (f * f_hi < 0.0) return make_hit(0.5 * (t_lo + t_hi));
+    if (fabs(f_hi) <= eps) return make_hit(t_hi);
+    return false;
+  }
+
+  for (int step = 0; step < 32; ++step) {
+    const bool at_end = t + fabs(f) >= t_hi;
+    const double t_next = at_end ? t_hi : t + fabs(f);
+    const double f_next = sdf_value_at(origin + t_next * dir, ie, planar, pp, pn, g, s);
+    if (fabs(f_next) <= eps) return make_hit(t_next);
+    if (f * f_next < 0.0) {
+      double a = t, b = t_next, fa = f;
+      for (int i = 0; i < 64; ++i) {
+        const double m = 0.5 * (a + b);
+        const double fm = sdf_value_at(origin + m * dir, ie, planar, pp, pn, g, s);
+        if (fabs(fm) <= eps) return make_hit(m);
+        if (fa * fm < 0.0) {
+          b = m;
+        } else {
+          a = m;
+          fa = fm;
+        }
+      }
+      return make_hit(0.5 * (a + b));
+    }
+    if (at_end) return false;
+    t = t_next;
+    f = f_next;
+  }
+  return false;
+}
+
+// project_to_surface (surface.cpp:136-162)
+__device__ inline bool project_to_surface(const V3& x, uint32_t ie, const GridView& g, const SceneView& s,
+                                          SurfaceHit* out) {
+  const double eps = g.hit_eps;
+  V3 p = x;
+  if (ie_planar(g, ie)) {
+    const V3 pp = ld3(g.ie_pp[ie]);
+    const V3 pn = ld3(g.ie_pn[ie]);
+    p = p - dot(p - pp, pn) * pn;
+    out->position = p;
+    out->normal = pn;
+    out->label = g.ie_label[ie];
+    out->distance = 0.0;
+    return true;
+  }
+  for (int i = 0; i < 16; ++i) {
+    const SurfaceEstimate est = estimate_surface(p, ie, g, s);
+    if (fabs(est.sdf) <= eps) {
+      out->position = p;
+      out->normal = est.n_bar;
+      out->label = g.ie_label[ie];
+      out->distance = 0.0;
+      return true;
+    }
+    p = p - est.sdf * est.n_bar;
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------------------------
+// GridWalker (tracer.cpp:18-92)
+struct Walker {
+  V3 o, d;
+  double t_end;
+  int v[3], step[3];
+  double t_next[3], delta[3];
+  double t_entry;
+  bool active;
+
+  __device__ __forceinline__ void init(const GridView& g, const V3& origin, const V3& dir, double t0, double t1) {
+    o = origin;
+    d = dir;
+    t_end = t1;
+    active = false;
+    double lo = t0, hi = t1;
+    const double od[3] = {o.x, o.y, o.z};
+    const double dd[3] = {d.x, d.y, d.z};
+    const double gd[3] = {g.origin.x, g.origin.y, g.origin.z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double bmin = gd[a];
+      const double bmax = gd[a] + static_cast<double>(g.dims[a]) * g.voxel_size;
+      if (fabs(dd[a]) < kTiny) {
+        if (od[a] < bmin || od[a] > bmax) return;
+        continue;
+      }
+      double ta = (bmin - od[a]) / dd[a];
+      double tb = (bmax - od[a]) / dd[a];
+      if (ta > tb) {
+        const double tmp = ta;
+        ta = tb;
+        tb = tmp;
+      }
+      lo = smax(lo, ta);
+      hi = smin(hi, tb);
+    }
+    if (lo > hi) return;
+    t_entry = lo;
+    const double p[3] = {od[0] + lo * dd[0], od[1] + lo * dd[1], od[2] + lo * dd[2]};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      v[a] = sclamp(static_cast<int>(floor((p[a] - gd[a]) / g.voxel_size)), 0, g.dims[a] - 1);
+      if (dd[a] > kTiny) {
+        step[a] = 1;
+        t_next[a] = ((gd[a] + static_cast<double>(v[a] + 1) * g.voxel_size) - od[a]) / dd[a];
+        delta[a] = g.voxel_size / dd[a];
+      } else if (dd[a] < -kTiny) {
+        step[a] = -1;
+        t_next[a] = ((gd[a] + static_cast<double>(v[a]) * g.voxel_size) - od[a]) / dd[a];
+        delta[a] = -g.voxel_size / dd[a];
+      } else {
+        step[a] = 0;
+        t_next[a] = __longlong_as_double(0x7ff0000000000000ll);
+        delta[a] = 0.0;
+      }
+    }
+    active = true;
+  }
+
+  // Returns the stepped axis, or -1 when the walk ended.
+  __device__ __forceinline__ int advance(const GridView& g) {
+    if (!active) return -1;
+    int axis = 0;
+    if (t_next[1] < t_next[axis]) axis = 1;
+    if (t_next[2] < t_next[axis]) axis = 2;
+    if (t_next[axis] > t_end) {
+      active = false;
+      return -1;
+    }
+    t_entry = t_next[axis];
+    v[axis] += step[axis];
+    if (v[axis] < 0 || v[axis] >= g.dims[axis]) {
+      active = false;
+      return -1;
+    }
+    t_next[axis] += delta[axis];
+    return axis;
+  }
+};
+
+// cone_intersects_sphere (tracer.cpp:129-136)
+__device__ __forceinline__ bool cone_intersects_sphere(const V3& o, const V3& d, double alpha, const V3& c,
+                                                       double r) {
+  const V3 vc = c - o;
+  const double dist = norm(vc);
+  if (dist <= r) return true;
+  const double beta = angle_between(vc, d);
+  return beta <= alpha + asin(smin(1.0, r / dist));
+}
+
+// segment_visible (tracer.cpp:138-205). The result is "no SurfacePoints IE other than
+// target_ie blocks the windowed span", an existential over the union of the walked
+// voxels' 27-neighbourhoods, so the visiting order is free. The reference dedups
+// cells with epoch stamps; here a plain DDA step along axis a only exposes the
+// 9-cell far slab of the new neighbourhood (voxel coordinates are monotone along
+// the walk), so the first voxel scans 27 cells and every later step 9.
+__device__ inline bool segment_visible(const V3& origin, const V3& target, uint32_t target_ie, const GridView& g,
+                                       const SceneView& s) {
+  const V3 diff = target - origin;
+  const double dist = norm(diff);
+  if (dist < kTiny) return true;
+  const V3 d = diff / dist;
+  const double er = g.sub_radius;
+  const double span = dist - 2.0 * er;
+  if (span <= 1e-9) return true;
+  const V3 o2 = origin + er * d;
+  const double cell_reach = g.voxel_radius + g.sub_radius;
+
+  Walker w;
+  w.init(g, origin, d, 0.0, dist);
+  int axis = -1;  // -1: full 27-neighbourhood
+  while (w.active) {
+    const int sa = axis;
+    const int lo0 = (sa == 0) ? w.step[0] : -1, hi0 = (sa == 0) ? w.step[0] : 1;
+    const int lo1 = (sa == 1) ? w.step[1] : -1, hi1 = (sa == 1) ? w.step[1] : 1;
+    const int lo2 = (sa == 2) ? w.step[2] : -1, hi2 = (sa == 2) ? w.step[2] : 1;
+    for (int oz = lo2; oz <= hi2; ++oz) {
+      for (int oy = lo1; oy <= hi1; ++oy) {
+        for (int ox = lo0; ox <= hi0; ++ox) {
+          const int nx = w.v[0] + ox, ny = w.v[1] + oy, nz = w.v[2] + oz;
+          if (!in_bounds(g, nx, ny, nz)) continue;
+          const int4 cell = g.cells[linear_index(g, nx, ny, nz)];
+          if (cell.x == cell.y) continue;
+          const V3 cc = voxel_center(g, nx, ny, nz);
+          const double tcc = sclamp(dot(cc - o2, d), 0.0, span);
+          if (norm((o2 + tcc * d) - cc) > cell_reach) continue;
+          for (uint32_t i = static_cast<uint32_t>(cell.x); i < static_cast<uint32_t>(cell.y); ++i) {
+            if ((g.ie_meta[i] & 3u) != kSurface) continue;
+            if (i == target_ie) continue;
+            const double4 sc4 = g.ie_sc[i];
+            const V3 sc = ld3(sc4);
+            const double tc = sclamp(dot(sc - o2, d), 0.0, span);
+            if (norm((o2 + tc * d) - sc) > sc4.w) continue;
+            SurfaceHit hit;
+            if (!march_segment(o2, d, i, g, s, span, &hit)) continue;
+            if (hit.distance <= 1e-9) continue;
+            if (hit.distance >= span - 1e-9) continue;
+            return false;
+          }
+        }
+      }
+    }
+    axis = w.advance(g);
+  }
+  return true;
+}
+
+}  // namespace pcr

@@ -1,0 +1,517 @@
+// pipeline.cu — run_pipeline_on_scene (proj/src/pipeline.cpp:99-212) over the
+// device stages, plus the host-side pieces of the reference contract that sit
+// outside the hot path: validate_scene (scene.cpp:31-91), dedup_by_label /
+// dedup_by_fresnel (refine.cpp:288-372), the final output order
+// (pipeline.cpp:194-207) and config_hash (pipeline.cpp:89-97).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <unordered_set>
+#include <vector>
+
+#include "host_alloc.hpp"
+#include "pipeline.hpp"
+#include "stages.cuh"
+#include "trace.cuh"
+
+namespace pcr {
+
+namespace {
+
+constexpr double kC = 299792458.0;
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+// ---- config -----------------------------------------------------------------------------
+uint64_t fnv1a(const char* s) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (; *s; ++s) {
+    h ^= static_cast<unsigned char>(*s);
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+// ---- validate_scene -------------------------------------------------------------------------
+struct Violation {
+  std::string rule, detail;
+  size_t index;
+};
+
+bool finite3(const double* p) { return std::isfinite(p[0]) && std::isfinite(p[1]) && std::isfinite(p[2]); }
+double norm3(const double* p) { return std::sqrt((p[0] * p[0] + p[1] * p[1]) + p[2] * p[2]); }
+
+// Returns the first violation in the reference's report order, if any.
+bool first_violation(const pcr_scene_desc& d, Violation& v) {
+  std::vector<Violation> out;
+  auto add = [&](const std::string& rule, size_t i, const std::string& detail) {
+    if (out.empty()) out.push_back({rule, detail, i});
+  };
+  const bool need_labels = d.n_edges > 0;
+  std::unordered_set<uint32_t> labels;
+  for (uint64_t i = 0; i < d.n_points; ++i) {
+    if (!finite3(d.point_position + 3 * i)) add("point_position_finite", i, "non-finite position");
+    const double nn = norm3(d.point_normal + 3 * i);
+    if (std::abs(nn - 1.0) > 1e-6) add("point_normal_unit", i, "normal length " + std::to_string(nn));
+    if (need_labels) labels.insert(d.point_label[i]);
+    if (!out.empty() && !need_labels) break;
+  }
+  for (uint32_t i = 0; i < d.n_edges; ++i) {
+    const double* g = d.edge_geometry + 12ull * i;
+    const V3 s = load3(g), e = load3(g + 3), na = load3(g + 6), nb = load3(g + 9);
+    const double len = norm(e - s);
+    if (!(len > 0.0)) {
+      add("edge_nondegenerate", i, "zero-length edge");
+      continue;
+    }
+    const V3 w = (e - s) / len;
+    if (std::abs(norm(na) - 1.0) > 1e-6) add("edge_normal_a_unit", i, "normal_a not unit");
+    if (std::abs(norm(nb) - 1.0) > 1e-6) add("edge_normal_b_unit", i, "normal_b not unit");
+    if (std::abs(dot(w, na)) > 1e-3) add("edge_normal_a_perpendicular", i, "w.n_a = " + std::to_string(dot(w, na)));
+    if (std::abs(dot(w, nb)) > 1e-3) add("edge_normal_b_perpendicular", i, "w.n_b = " + std::to_string(dot(w, nb)));
+    if (norm(na - nb) < 1e-9) add("edge_wedge_defined", i, "adjacent normals coincide");
+    if (labels.count(d.edge_label[i]) > 0)
+      add("edge_label_disjoint", i,
+          "edge label " + std::to_string(d.edge_label[i]) + " collides with a surface label");
+  }
+  auto radios = [&](const double* pos, const uint32_t* id, uint32_t n, const char* kind) {
+    std::unordered_set<uint32_t> ids;
+    for (uint32_t i = 0; i < n; ++i) {
+      if (!finite3(pos + 3ull * i)) add(std::string(kind) + "_position_finite", i, "non-finite position");
+      if (!ids.insert(id[i]).second) add(std::string(kind) + "_id_unique", i, "duplicate id " + std::to_string(id[i]));
+    }
+  };
+  radios(d.tx_position, d.tx_id, d.n_tx, "tx");
+  radios(d.rx_position, d.rx_id, d.n_rx, "rx");
+  if (d.n_tx == 0) add("has_transmitter", 0, "no transmitters");
+  if (d.n_rx == 0) add("has_receiver", 0, "no receivers");
+  if (!(d.carrier_frequency_hz > 0.0)) add("carrier_frequency_positive", 0, "frequency must be > 0");
+  if (out.empty()) return false;
+  v = out.front();
+  return true;
+}
+
+// ---- exact paths, dedup, final order ----------------------------------------------------------
+struct It {
+  uint8_t kind;
+  V3 pos, nrm;
+  uint32_t label, ie, edge;
+};
+struct EP {
+  uint32_t tx_id, rx_id;
+  V3 tx, rx;
+  std::vector<It> its;
+  double total_length, delay, gnorm;
+  bool converged;
+};
+
+bool lex_less(const V3& a, const V3& b) {
+  if (a.x != b.x) return a.x < b.x;
+  if (a.y != b.y) return a.y < b.y;
+  return a.z < b.z;
+}
+bool positions_lex_less(const EP& a, const EP& b) {
+  for (size_t k = 0; k < std::min(a.its.size(), b.its.size()); ++k)
+    if (a.its[k].pos != b.its[k].pos) return lex_less(a.its[k].pos, b.its[k].pos);
+  return a.its.size() < b.its.size();
+}
+void sort_by_delay(std::vector<EP>& v) {
+  std::sort(v.begin(), v.end(), [](const EP& a, const EP& b) {
+    if (a.delay != b.delay) return a.delay < b.delay;
+    if (a.tx_id != b.tx_id) return a.tx_id < b.tx_id;
+    if (a.rx_id != b.rx_id) return a.rx_id < b.rx_id;
+    return positions_lex_less(a, b);
+  });
+}
+std::vector<int> kinds(const EP& p) {
+  std::vector<int> k;
+  for (const It& i : p.its) k.push_back(i.kind);
+  return k;
+}
+std::vector<uint32_t> labels_of(const EP& p) {
+  std::vector<uint32_t> k;
+  for (const It& i : p.its) k.push_back(i.label);
+  return k;
+}
+
+// dedup_by_label (refine.cpp:324-343)
+std::vector<EP> dedup_by_label(std::vector<EP> paths) {
+  using Key = std::tuple<uint32_t, uint32_t, std::vector<int>, std::vector<uint32_t>>;
+  std::map<Key, size_t> best;
+  for (size_t i = 0; i < paths.size(); ++i) {
+    Key key{paths[i].tx_id, paths[i].rx_id, kinds(paths[i]), labels_of(paths[i])};
+    auto [it, inserted] = best.try_emplace(std::move(key), i);
+    if (inserted) continue;
+    const EP& cur = paths[it->second];
+    const EP& cand = paths[i];
+    if (cand.total_length < cur.total_length ||
+        (cand.total_length == cur.total_length && positions_lex_less(cand, cur)))
+      it->second = i;
+  }
+  std::vector<EP> out;
+  out.reserve(best.size());
+  for (const auto& kv : best) out.push_back(paths[kv.second]);
+  sort_by_delay(out);
+  return out;
+}
+
+// dedup_by_fresnel (refine.cpp:345-372)
+std::vector<EP> dedup_by_fresnel(std::vector<EP> paths, double freq) {
+  const double lambda = kC / freq;
+  sort_by_delay(paths);
+  std::vector<EP> kept;
+  for (EP& p : paths) {
+    bool dup = false;
+    for (const EP& q : kept) {
+      if (q.tx_id != p.tx_id || q.rx_id != p.rx_id) continue;
+      if (kinds(q) != kinds(p)) continue;
+      bool inside = true;
+      for (size_t k = 0; k < p.its.size() && inside; ++k) {
+        const V3 a = k == 0 ? q.tx : q.its[k - 1].pos;
+        const V3 b = q.its[k].pos;
+        const V3& pt = p.its[k].pos;
+        inside = norm(pt - a) + norm(pt - b) <= norm(b - a) + 0.5 * lambda;
+      }
+      if (inside) {
+        dup = true;
+        break;
+      }
+    }
+    if (!dup) kept.push_back(std::move(p));
+  }
+  return kept;
+}
+
+void final_sort(std::vector<EP>& v) {
+  std::sort(v.begin(), v.end(), [](const EP& a, const EP& b) {
+    if (a.tx_id != b.tx_id) return a.tx_id < b.tx_id;
+    if (a.rx_id != b.rx_id) return a.rx_id < b.rx_id;
+    if (a.delay != b.delay) return a.delay < b.delay;
+    if (a.its.size() != b.its.size()) return a.its.size() < b.its.size();
+    for (size_t k = 0; k < a.its.size(); ++k)
+      if (a.its[k].pos != b.its[k].pos) return lex_less(a.its[k].pos, b.its[k].pos);
+    return false;
+  });
+}
+
+// ---- combined candidate set on the device -----------------------------------------------------
+struct CandSet {
+  uint32_t n = 0, stride = 1;
+  DBuf<uint32_t> tx_id, rx_id, n_inter, label, ie, edge;
+  DBuf<uint8_t> kind;
+  DBuf<double> tx_pos, rx_pos, length, pos, nrm;
+};
+
+__global__ void los_rows_kernel(const uint32_t* __restrict__ los_ie, uint32_t n, GridView g, V3 tx, uint32_t tx_id,
+                                uint32_t row0, uint32_t* rx_id, double* rx_pos, double* length, uint32_t* n_inter,
+                                uint32_t* txid, double* txpos) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint32_t i = los_ie[k];
+  const V3 rp = ld3(g.ie_rp[i]);
+  const uint32_t r = row0 + k;
+  rx_id[r] = g.ie_rx[i];
+  store3(rx_pos + 3ull * r, rp);
+  length[r] = norm(rp - tx);
+  n_inter[r] = 0;
+  txid[r] = tx_id;
+  store3(txpos + 3ull * r, tx);
+}
+
+__global__ void tx_rows_kernel(uint32_t n, uint32_t row0, V3 tx, uint32_t tx_id, uint32_t* txid, double* txpos) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  txid[row0 + k] = tx_id;
+  store3(txpos + 3ull * (row0 + k), tx);
+}
+
+unsigned nb(uint64_t n, unsigned t = 256) { return static_cast<unsigned>((n + t - 1) / t ? (n + t - 1) / t : 1); }
+
+void put_paths(pcr_paths* P, const std::vector<EP>& v) {
+  for (size_t i = 0; i < v.size(); ++i) {
+    const EP& e = v[i];
+    P->tx_id[i] = e.tx_id;
+    P->rx_id[i] = e.rx_id;
+    store3(P->tx_position + 3 * i, e.tx);
+    store3(P->rx_position + 3 * i, e.rx);
+    P->length[i] = e.total_length;
+    P->delay[i] = e.delay;
+    P->converged[i] = e.converged ? 1 : 0;
+    P->gradient_norm[i] = e.gnorm;
+    P->n_inter[i] = static_cast<uint32_t>(e.its.size());
+    for (size_t k = 0; k < e.its.size(); ++k) {
+      const size_t j = i * P->stride + k;
+      P->kind[j] = e.its[k].kind;
+      store3(P->position + 3 * j, e.its[k].pos);
+      P->label[j] = e.its[k].label;
+      store3(P->normal + 3 * j, e.its[k].nrm);
+      P->ie_index[j] = e.its[k].ie;
+      P->edge_index[j] = e.its[k].edge;
+    }
+  }
+}
+
+}  // namespace
+
+uint64_t config_hash(const pcr_run_config& c) {
+  char buf[512];
+  std::snprintf(buf, sizeof(buf), "%.17g|%.17g|%d|%d|%d|%d|%.17g|%d|%.17g|%d|%.17g|%d", c.carrier_frequency_hz,
+                c.voxel_size_m, c.division_factor, c.kappa, c.max_interactions, c.max_diffractions,
+                c.cone_apex_angle_deg, c.diffraction_ray_count, c.delta, c.rho, c.step_size,
+                c.fresnel_enabled ? 1 : 0);
+  return fnv1a(buf);
+}
+
+void run_config_defaults(pcr_run_config* c) {
+  c->carrier_frequency_hz = 60e9;
+  c->voxel_size_m = 0.5;
+  c->division_factor = 2;
+  c->kappa = 100;
+  c->max_interactions = 5;
+  c->max_diffractions = 1;
+  c->cone_apex_angle_deg = 1.0;
+  c->diffraction_ray_count = 360;
+  c->delta = 1e-4;
+  c->rho = 2000;
+  c->step_size = 0.5;
+  c->seed = 1;
+  c->thread_count = 0;
+  c->fresnel_enabled = 1;
+}
+
+void api_run_pipeline_on_scene(Ctx& ctx, const pcr_scene_desc& desc, const pcr_run_config& cfg, pcr_summary** out) {
+  cudaStream_t s = ctx.stream;
+  pcr_summary* S = halloc<pcr_summary>(1);
+  auto fail = [&](const char* stage, const std::exception& e) {
+    std::free(S);
+    const Error* pe = dynamic_cast<const Error*>(&e);
+    std::string msg = e.what();
+    // device stages already prefix "trace: " style messages for their own errors
+    if (msg.rfind(std::string(stage) + ": ", 0) != 0) msg = std::string(stage) + ": " + msg;
+    throw Error(pe ? pe->code : PCR_ERR_RUNTIME, msg);
+  };
+  auto timing = [&](const char* name, double sec) {
+    if (S->n_timings < PCR_MAX_STAGES) {
+      std::snprintf(S->timing_stage[S->n_timings], 16, "%s", name);
+      S->timing_seconds[S->n_timings++] = sec;
+    }
+  };
+  S->hash = config_hash(cfg);
+  S->point_count = desc.n_points;
+  S->edge_count = desc.n_edges;
+
+  auto t0 = Clock::now();
+  Violation v;
+  if (first_violation(desc, v)) {
+    std::free(S);
+    throw Error(PCR_ERR_RUNTIME, "validate: " + v.rule + " (" + v.detail + ")");
+  }
+  timing("validate", since(t0));
+
+  // upload + voxelize
+  t0 = Clock::now();
+  SceneDev scene;
+  GridDev grid;
+  try {
+    const size_t n = desc.n_points;
+    scene.n_points = n;
+    scene.pos.alloc(3 * n + 3, s);
+    scene.nrm.alloc(3 * n + 3, s);
+    scene.label.alloc(n + 1, s);
+    h2d(scene.pos.get(), desc.point_position, 3 * n, s);
+    h2d(scene.nrm.get(), desc.point_normal, 3 * n, s);
+    h2d(scene.label.get(), desc.point_label, n, s);
+    scene.n_edges = desc.n_edges;
+    scene.h_edges.assign(desc.edge_geometry, desc.edge_geometry + 12ull * desc.n_edges);
+    scene.h_edge_label.assign(desc.edge_label, desc.edge_label + desc.n_edges);
+    scene.edges.alloc(12ull * desc.n_edges + 12, s);
+    scene.edge_label.alloc(desc.n_edges + 1ull, s);
+    h2d(scene.edges.get(), scene.h_edges.data(), scene.h_edges.size(), s);
+    h2d(scene.edge_label.get(), scene.h_edge_label.data(), scene.h_edge_label.size(), s);
+    scene.h_tx.assign(desc.tx_position, desc.tx_position + 3ull * desc.n_tx);
+    scene.h_tx_id.assign(desc.tx_id, desc.tx_id + desc.n_tx);
+    scene.h_rx.assign(desc.rx_position, desc.rx_position + 3ull * desc.n_rx);
+    scene.h_rx_id.assign(desc.rx_id, desc.rx_id + desc.n_rx);
+    scene.rx_pos.alloc(3ull * desc.n_rx + 3, s);
+    scene.rx_id.alloc(desc.n_rx + 1ull, s);
+    h2d(scene.rx_pos.get(), scene.h_rx.data(), scene.h_rx.size(), s);
+    h2d(scene.rx_id.get(), scene.h_rx_id.data(), scene.h_rx_id.size(), s);
+    scene.carrier_frequency_hz = desc.carrier_frequency_hz;
+    build_grid_device(ctx, scene, cfg.voxel_size_m, cfg.division_factor, uint64_t(1) << 27, grid);
+  } catch (const std::exception& e) {
+    fail("voxelize", e);
+  }
+  S->ie_count = grid.n_ies;
+  for (int a = 0; a < 3; ++a) S->grid_dims[a] = grid.dims[a];
+  timing("voxelize", since(t0));
+
+  // trace
+  t0 = Clock::now();
+  pcr_trace_params tp;
+  tp.max_interactions = cfg.max_interactions;
+  tp.kappa = cfg.kappa;
+  tp.cone_apex_angle = cfg.cone_apex_angle_deg * 3.141592653589793238462643383279502884 / 180.0;
+  tp.diffraction_ray_count = cfg.diffraction_ray_count;
+  tp.max_diffractions = cfg.max_diffractions;
+  const uint32_t stride = static_cast<uint32_t>(std::max(1, cfg.max_interactions));
+  CandSet cs;
+  cs.stride = stride;
+  try {
+    std::vector<TxDev> txs(desc.n_tx);
+    std::vector<CandDev> props(desc.n_tx);
+    TraceStats st;
+    uint64_t total = 0;
+    for (uint32_t t = 0; t < desc.n_tx; ++t) {
+      transmission_device(ctx, grid, scene, t, txs[t]);
+      propagate_device(ctx, grid, scene, t, txs[t].hit_ie.get(), txs[t].hit_kind.get(), txs[t].hit_pos.get(),
+                       txs[t].hit_nrm.get(), txs[t].hit_inc.get(), txs[t].n_hits, tp, props[t], st);
+      txs[t].hit_ie.release();
+      txs[t].hit_kind.release();
+      txs[t].hit_pos.release();
+      txs[t].hit_nrm.release();
+      txs[t].hit_inc.release();
+      total += txs[t].n_los + props[t].n;
+      S->transmission_rays += grid.n_ies;
+      S->visibility_tests += grid.n_ies;
+    }
+    S->cone_traces = st.cone_traces;
+    S->visibility_tests += st.visibility_tests;
+    if (total > 0xffffffffull) throw Error(PCR_ERR_NOMEM, "too many candidates");
+    cs.n = static_cast<uint32_t>(total);
+    const size_t m = total ? total : 1, ms = m * stride;
+    cs.tx_id.alloc(m, s);
+    cs.rx_id.alloc(m, s);
+    cs.n_inter.alloc(m, s);
+    cs.label.alloc(ms, s);
+    cs.ie.alloc(ms, s);
+    cs.edge.alloc(ms, s);
+    cs.kind.alloc(ms, s);
+    cs.tx_pos.alloc(3 * m, s);
+    cs.rx_pos.alloc(3 * m, s);
+    cs.length.alloc(m, s);
+    cs.pos.alloc(3 * ms, s);
+    cs.nrm.alloc(3 * ms, s);
+    PCR_CUDA(cudaMemsetAsync(cs.label.get(), 0, ms * sizeof(uint32_t), s));
+    PCR_CUDA(cudaMemsetAsync(cs.ie.get(), 0, ms * sizeof(uint32_t), s));
+    PCR_CUDA(cudaMemsetAsync(cs.edge.get(), 0, ms * sizeof(uint32_t), s));
+    PCR_CUDA(cudaMemsetAsync(cs.kind.get(), 0, ms, s));
+    PCR_CUDA(cudaMemsetAsync(cs.pos.get(), 0, 3 * ms * sizeof(double), s));
+    PCR_CUDA(cudaMemsetAsync(cs.nrm.get(), 0, 3 * ms * sizeof(double), s));
+    uint32_t row = 0;
+    const GridView gv = grid.view();
+    for (uint32_t t = 0; t < desc.n_tx; ++t) {
+      const V3 txp = load3(desc.tx_position + 3ull * t);
+      if (txs[t].n_los) {
+        count_launch();
+        los_rows_kernel<<<nb(txs[t].n_los), 256, 0, s>>>(txs[t].los_ie.get(), txs[t].n_los, gv, txp, desc.tx_id[t], row,
+                                                          cs.rx_id.get(), cs.rx_pos.get(), cs.length.get(),
+                                                          cs.n_inter.get(), cs.tx_id.get(), cs.tx_pos.get());
+        PCR_LAUNCH_CHECK();
+        row += txs[t].n_los;
+      }
+      const CandDev& c = props[t];
+      if (c.n) {
+        PCR_CUDA(cudaMemcpyAsync(cs.rx_id.get() + row, c.rx_id.get(), c.n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        PCR_CUDA(cudaMemcpyAsync(cs.n_inter.get() + row, c.n_inter.get(), c.n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        PCR_CUDA(cudaMemcpyAsync(cs.rx_pos.get() + 3ull * row, c.rx_pos.get(), 3ull * c.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        PCR_CUDA(cudaMemcpyAsync(cs.length.get() + row, c.length.get(), c.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        const size_t q = static_cast<size_t>(row) * stride, cnt = static_cast<size_t>(c.n) * stride;
+        PCR_CUDA(cudaMemcpyAsync(cs.label.get() + q, c.label.get(), cnt * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        PCR_CUDA(cudaMemcpyAsync(cs.ie.get() + q, c.ie.get(), cnt * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        PCR_CUDA(cudaMemcpyAsync(cs.edge.get() + q, c.edge.get(), cnt * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        PCR_CUDA(cudaMemcpyAsync(cs.kind.get() + q, c.kind.get(), cnt, cudaMemcpyDeviceToDevice, s));
+        PCR_CUDA(cudaMemcpyAsync(cs.pos.get() + 3 * q, c.pos.get(), 3 * cnt * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        PCR_CUDA(cudaMemcpyAsync(cs.nrm.get() + 3 * q, c.nrm.get(), 3 * cnt * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        count_launch();
+        tx_rows_kernel<<<nb(c.n), 256, 0, s>>>(c.n, row, txp, desc.tx_id[t], cs.tx_id.get(), cs.tx_pos.get());
+        PCR_LAUNCH_CHECK();
+        row += c.n;
+      }
+    }
+    PCR_CUDA(cudaStreamSynchronize(s));
+  } catch (const std::exception& e) {
+    fail("trace", e);
+  }
+  S->coarse_paths = cs.n;
+  timing("trace", since(t0));
+
+  // refine
+  t0 = Clock::now();
+  std::vector<EP> exact;
+  try {
+    pcr_refine_params rp{cfg.delta, cfg.rho, cfg.step_size, cfg.fresnel_enabled};
+    RefineDevIn in{cs.n,         stride,        cs.tx_pos.get(), cs.rx_pos.get(), cs.pos.get(), cs.nrm.get(),
+                   cs.length.get(), cs.n_inter.get(), cs.label.get(), cs.edge.get(), cs.kind.get()};
+    RefineDevOut ro;
+    refine_device(ctx, grid, scene, in, rp, ro);
+    const size_t n = cs.n, ms = n * stride;
+    std::vector<uint8_t> has(n), kind(ms);
+    std::vector<int32_t> reason(n);
+    std::vector<uint32_t> txid(n), rxid(n), ni(n), lab(ms), ie(ms), ed(ms), iters(n);
+    std::vector<double> txp(3 * n), rxp(3 * n), pos(3 * ms), nrm(3 * ms), len(n), del(n), gn(n);
+    d2h(has.data(), ro.has_path.get(), n, s);
+    d2h(reason.data(), ro.reason.get(), n, s);
+    d2h(iters.data(), ro.iters.get(), n, s);
+    d2h(txid.data(), cs.tx_id.get(), n, s);
+    d2h(rxid.data(), cs.rx_id.get(), n, s);
+    d2h(ni.data(), cs.n_inter.get(), n, s);
+    d2h(kind.data(), cs.kind.get(), ms, s);
+    d2h(ie.data(), cs.ie.get(), ms, s);
+    d2h(ed.data(), cs.edge.get(), ms, s);
+    d2h(txp.data(), cs.tx_pos.get(), 3 * n, s);
+    d2h(rxp.data(), cs.rx_pos.get(), 3 * n, s);
+    d2h(pos.data(), ro.pos.get(), 3 * ms, s);
+    d2h(nrm.data(), ro.nrm.get(), 3 * ms, s);
+    d2h(lab.data(), ro.label.get(), ms, s);
+    d2h(len.data(), ro.length.get(), n, s);
+    d2h(del.data(), ro.delay.get(), n, s);
+    d2h(gn.data(), ro.gnorm.get(), n, s);
+    PCR_CUDA(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < n; ++i) {
+      S->refine_iterations += iters[i];
+      if (!has[i]) {
+        ++S->rejected[reason[i] & 3];
+        continue;
+      }
+      EP e;
+      e.tx_id = txid[i];
+      e.rx_id = rxid[i];
+      e.tx = load3(&txp[3 * i]);
+      e.rx = load3(&rxp[3 * i]);
+      e.total_length = len[i];
+      e.delay = del[i];
+      e.gnorm = gn[i];
+      e.converged = true;
+      for (uint32_t q = 0; q < ni[i]; ++q) {
+        const size_t j = i * stride + q;
+        e.its.push_back(It{kind[j], load3(&pos[3 * j]), load3(&nrm[3 * j]), lab[j], ie[j], ed[j]});
+      }
+      exact.push_back(std::move(e));
+    }
+  } catch (const std::exception& e) {
+    fail("refine", e);
+  }
+  S->refined_paths = exact.size();
+  timing("refine", since(t0));
+
+  t0 = Clock::now();
+  exact = dedup_by_label(std::move(exact));
+  if (cfg.fresnel_enabled) exact = dedup_by_fresnel(std::move(exact), cfg.carrier_frequency_hz);
+  final_sort(exact);
+  S->exact_paths = exact.size();
+  size_t st = 1;
+  for (const EP& e : exact) st = std::max(st, e.its.size());
+  pcr_paths* P = alloc_paths(exact.size(), static_cast<uint32_t>(st));
+  put_paths(P, exact);
+  S->paths = *P;
+  std::free(P);
+  timing("dedup", since(t0));
+  *out = S;
+}
+
+}  // namespace pcr

@@ -1,0 +1,26 @@
+// pipeline.hpp — host-side orchestration entry points behind the C ABI.
+#pragma once
+
+#include "../../include/pcray_b200.h"
+#include "device_state.cuh"
+
+namespace pcr {
+
+// stage 2 (trace.cu)
+void api_transmission(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint32_t tx_index,
+                      const pcr_trace_params& p, pcr_paths** los_out, pcr_initial_hits** hits_out);
+void api_propagate(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint32_t tx_index,
+                   const pcr_initial_hits& hits, const pcr_trace_params& p, pcr_paths** out);
+void api_cone_trace_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const pcr_ray_desc* rays,
+                          uint64_t n_rays, bool want_debug, pcr_receptions** out);
+void api_segment_visible_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const double* origin,
+                               const double* target, const uint32_t* target_ie, uint64_t n, uint8_t* visible_out);
+// stage 3 (refine.cu)
+void api_refine_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const pcr_paths& cands,
+                      const pcr_refine_params& p, pcr_outcomes** out);
+// pipeline (pipeline.cu)
+void api_run_pipeline_on_scene(Ctx& ctx, const pcr_scene_desc& desc, const pcr_run_config& cfg, pcr_summary** out);
+uint64_t config_hash(const pcr_run_config& c);
+void run_config_defaults(pcr_run_config* c);
+
+}  // namespace pcr

@@ -1,0 +1,435 @@
+// refine.cu — stage 3: refine_path (proj/src/refine.cpp:189-286) on the device,
+// one thread per coarse path, FP64 in the reference's operation order.
+//
+// Per iteration: local_gradients (:167-187), backtracking with up to 9 trial steps
+// (:209-232), front-to-back reprojection of reflection nodes (:234-250) through
+// surface_ies_near (:34-52) + march_segment / project_to_surface + polish (:62-130).
+// Shortcut (bit-exact): when no trial step is accepted the state is unchanged, so
+// every remaining iteration repeats the same computation and the outcome is
+// not_converged; the kernel stops there instead of spinning to rho.
+#include <cstring>
+#include <vector>
+
+#include "host_alloc.hpp"
+#include "pipeline.hpp"
+#include "stages.cuh"
+#include "trace.cuh"
+
+namespace pcr {
+
+constexpr double kSpeedOfLight = 299792458.0;
+
+namespace {
+
+struct RNode {
+  V3 c, a, b, n;  // reflection: c, u, v, normal; diffraction: c, w, -, -
+  double p0, p1;  // reflection: r, s; diffraction: t, -
+  double lo, hi;  // diffraction t range
+  uint32_t label, edge;
+  uint8_t kind;
+};
+
+__device__ __forceinline__ V3 node_point(const RNode& nd, double p0, double p1) {
+  return nd.kind == 0 ? (nd.c + p0 * nd.a) + p1 * nd.b : nd.c + p0 * nd.a;
+}
+
+__device__ __forceinline__ double chain_len(const V3& tx, const V3* pts, int n, const V3& rx) {
+  V3 prev = tx;
+  double len = 0.0;
+  for (int k = 0; k < n; ++k) {
+    len += norm(pts[k] - prev);
+    prev = pts[k];
+  }
+  return len + norm(rx - prev);
+}
+
+struct Reproj {
+  V3 pos, nrm;
+  uint32_t label;
+};
+
+// polish (refine.cpp:62-75)
+__device__ void polish(Reproj& re, uint32_t ie, const GridView& g, const SceneView& s) {
+  if (ie_planar(g, ie)) {
+    const V3 pp = ld3(g.ie_pp[ie]), pn = ld3(g.ie_pn[ie]);
+    re.pos = re.pos - dot(re.pos - pp, pn) * pn;
+    re.nrm = pn;
+    return;
+  }
+  for (int i = 0; i < 4; ++i) {
+    const SurfaceEstimate est = estimate_surface(re.pos, ie, g, s);
+    re.pos = re.pos - est.sdf * est.n_bar;
+    re.nrm = est.n_bar;
+    if (fabs(est.sdf) <= 1e-12) break;
+  }
+}
+
+__device__ __forceinline__ int voxel_floor(double p, double o, double vs) {
+  return static_cast<int>(floor((p - o) / vs));
+}
+
+// reproject (refine.cpp:80-130) with surface_ies_near (:34-52) scanned in place.
+__device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, const GridView& g, const SceneView& s,
+                          Reproj& out) {
+  const V3 diff = predicted - prev;
+  const double dist = norm(diff);
+  if (dist < kTiny) return false;
+  const V3 dir = diff / dist;
+  const double radius = 2.0 * g.sub_edge;
+  const double pc[3] = {predicted.x, predicted.y, predicted.z};
+  const double oc[3] = {g.origin.x, g.origin.y, g.origin.z};
+  int lo[3], hi[3];
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = smin(smax(voxel_floor(pc[a] - radius, oc[a], g.voxel_size), 0), g.dims[a] - 1);
+    hi[a] = smin(smax(voxel_floor(pc[a] + radius, oc[a], g.voxel_size), 0), g.dims[a] - 1);
+  }
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool same = pass == 0;
+    bool found = false;
+    uint32_t best_ie = 0;
+    double best_t = 1.7976931348623157e308;
+    Reproj best;
+    for (int z = lo[2]; z <= hi[2]; ++z)
+      for (int y = lo[1]; y <= hi[1]; ++y)
+        for (int x = lo[0]; x <= hi[0]; ++x) {
+          const int4 cell = g.cells[linear_index(g, x, y, z)];
+          for (uint32_t i = static_cast<uint32_t>(cell.x); i < static_cast<uint32_t>(cell.y); ++i) {
+            if ((g.ie_meta[i] & 3u) != kSurface) continue;
+            const double4 sc4 = g.ie_sc[i];
+            if (!(norm(ld3(sc4) - predicted) <= radius + sc4.w)) continue;
+            if (same != (g.ie_label[i] == label)) continue;
+            SurfaceHit hit;
+            if (!march_segment(prev, dir, i, g, s, inf, &hit)) continue;
+            if (hit.distance >= best_t) continue;
+            best_t = hit.distance;
+            best = Reproj{hit.position, hit.normal, g.ie_label[i]};
+            best_ie = i;
+            found = true;
+          }
+        }
+    if (found) {
+      polish(best, best_ie, g, s);
+      out = best;
+      return true;
+    }
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool same = pass == 0;
+    bool found = false;
+    uint32_t best_ie = 0;
+    double best_d = 1.7976931348623157e308;
+    Reproj best;
+    for (int z = lo[2]; z <= hi[2]; ++z)
+      for (int y = lo[1]; y <= hi[1]; ++y)
+        for (int x = lo[0]; x <= hi[0]; ++x) {
+          const int4 cell = g.cells[linear_index(g, x, y, z)];
+          for (uint32_t i = static_cast<uint32_t>(cell.x); i < static_cast<uint32_t>(cell.y); ++i) {
+            if ((g.ie_meta[i] & 3u) != kSurface) continue;
+            const double4 sc4 = g.ie_sc[i];
+            const V3 sc = ld3(sc4);
+            if (!(norm(sc - predicted) <= radius + sc4.w)) continue;
+            if (same != (g.ie_label[i] == label)) continue;
+            const double d = norm(sc - predicted);
+            if (d >= best_d) continue;
+            SurfaceHit hit;
+            if (!project_to_surface(predicted, i, g, s, &hit)) continue;
+            best_d = d;
+            best = Reproj{hit.position, hit.normal, g.ie_label[i]};
+            best_ie = i;
+            found = true;
+          }
+        }
+    if (found) {
+      polish(best, best_ie, g, s);
+      out = best;
+      return true;
+    }
+  }
+  return false;
+}
+
+struct CandIn {
+  uint32_t stride;
+  const double* tx;
+  const double* rx;
+  const uint32_t* n_inter;
+  const uint8_t* kind;
+  const double* pos;
+  const uint32_t* label;
+  const double* nrm;
+  const uint32_t* edge;
+  const double* coarse_length;
+};
+
+struct RefOut {
+  int32_t* reason;
+  uint8_t* has_path;
+  double* pos;
+  double* nrm;
+  uint32_t* label;
+  double* length;
+  double* delay;
+  double* gnorm;
+  uint32_t* iters;
+};
+
+__global__ void __launch_bounds__(128) refine_kernel(CandIn in, uint32_t n, GridView g, SceneView s, double delta,
+                                                     int rho, double step_size, RefOut o) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int d = static_cast<int>(in.n_inter[k]);
+  const V3 tx = load3(in.tx + 3ull * k), rx = load3(in.rx + 3ull * k);
+  o.has_path[k] = 0;
+  o.iters[k] = 0;
+  if (d == 0) {
+    // LOS passes through (pipeline.cpp:160-170)
+    o.has_path[k] = 1;
+    o.reason[k] = PCR_NOT_CONVERGED;
+    o.length[k] = in.coarse_length[k];
+    o.delay[k] = in.coarse_length[k] / kSpeedOfLight;
+    o.gnorm[k] = 0.0;
+    return;
+  }
+  RNode nd[kMaxDepth];
+  // make_path_state (refine.cpp:134-161)
+  for (int q = 0; q < d; ++q) {
+    const size_t j = static_cast<size_t>(k) * in.stride + q;
+    RNode& x = nd[q];
+    x.kind = in.kind[j];
+    x.c = load3(in.pos + 3 * j);
+    x.label = in.label[j];
+    x.edge = in.edge[j];
+    x.p0 = 0.0;
+    x.p1 = 0.0;
+    if (x.kind == 0) {
+      x.n = load3(in.nrm + 3 * j);
+      local_frame(x.n, x.a, x.b);
+      x.lo = x.hi = 0.0;
+    } else {
+      const double* e = s.edges + 12ull * x.edge;
+      const V3 es = load3(e), ee = load3(e + 3);
+      x.a = normalized(ee - es);
+      x.lo = dot(es - x.c, x.a);
+      x.hi = dot(ee - x.c, x.a);
+      x.b = V3{0, 1, 0};
+      x.n = V3{0, 0, 1};
+    }
+  }
+  V3 pts[kMaxDepth];
+  for (int q = 0; q < d; ++q) pts[q] = node_point(nd[q], nd[q].p0, nd[q].p1);
+  double f = chain_len(tx, pts, d, rx);
+  double gnorm = 0.0;
+  bool converged = false;
+  int iter = 0;
+  for (; iter < rho; ++iter) {
+    // local_gradients
+    double gr[2 * kMaxDepth];
+    int ng = 0;
+    for (int q = 0; q < d; ++q) {
+      const V3 prev = q == 0 ? tx : pts[q - 1];
+      const V3 next = q + 1 == d ? rx : pts[q + 1];
+      const V3 dp = pts[q] - prev;
+      const V3 dn = pts[q] - next;
+      const double lp = norm(dp), ln = norm(dn);
+      if (lp < kTiny || ln < kTiny) {
+        o.reason[k] = PCR_DEGENERATE;
+        o.iters[k] = iter + 1;
+        return;
+      }
+      const V3 e_sum = dp / lp + dn / ln;
+      if (nd[q].kind == 0) {
+        gr[ng++] = dot(nd[q].a, e_sum);
+        gr[ng++] = dot(nd[q].b, e_sum);
+      } else {
+        gr[ng++] = dot(nd[q].a, e_sum);
+      }
+    }
+    gnorm = 0.0;
+    for (int q = 0; q < ng; ++q) gnorm += gr[q] * gr[q];
+    gnorm = sqrt(gnorm);
+    if (gnorm < delta) {
+      converged = true;
+      break;
+    }
+    // backtracking (refine.cpp:209-232)
+    double step = step_size;
+    bool accepted = false;
+    double tp0[kMaxDepth], tp1[kMaxDepth];
+    for (int h = 0; h <= 8; ++h) {
+      int gi = 0;
+      V3 tpts[kMaxDepth];
+      for (int q = 0; q < d; ++q) {
+        if (nd[q].kind == 0) {
+          tp0[q] = nd[q].p0 - step * gr[gi++];
+          tp1[q] = nd[q].p1 - step * gr[gi++];
+        } else {
+          tp0[q] = sclamp(nd[q].p0 - step * gr[gi++], nd[q].lo, nd[q].hi);
+          tp1[q] = nd[q].p1;
+        }
+        tpts[q] = node_point(nd[q], tp0[q], tp1[q]);
+      }
+      if (chain_len(tx, tpts, d, rx) <= f + 1e-15) {
+        accepted = true;
+        break;
+      }
+      step *= 0.5;
+    }
+    if (!accepted) {
+      iter = rho;  // fixed point: every remaining iteration repeats this one
+      break;
+    }
+    for (int q = 0; q < d; ++q) {
+      nd[q].p0 = tp0[q];
+      nd[q].p1 = tp1[q];
+    }
+    // reprojection, front to back (refine.cpp:234-250)
+    for (int q = 0; q < d; ++q) {
+      if (nd[q].kind != 0) continue;
+      const V3 prev = q == 0 ? tx : node_point(nd[q - 1], nd[q - 1].p0, nd[q - 1].p1);
+      const V3 predicted = node_point(nd[q], nd[q].p0, nd[q].p1);
+      Reproj re;
+      if (!reproject(prev, predicted, nd[q].label, g, s, re)) {
+        o.reason[k] = PCR_RAY_MISSED;
+        o.iters[k] = iter + 1;
+        return;
+      }
+      nd[q].c = re.pos;
+      nd[q].n = re.nrm;
+      local_frame(re.nrm, nd[q].a, nd[q].b);
+      nd[q].p0 = 0.0;
+      nd[q].p1 = 0.0;
+      nd[q].label = re.label;
+    }
+    for (int q = 0; q < d; ++q) pts[q] = node_point(nd[q], nd[q].p0, nd[q].p1);
+    f = chain_len(tx, pts, d, rx);
+  }
+  o.iters[k] = static_cast<uint32_t>(converged ? iter + 1 : iter);
+  if (!converged) {
+    o.reason[k] = PCR_NOT_CONVERGED;
+    return;
+  }
+  // final per-segment visibility (refine.cpp:256-265)
+  V3 prev = tx;
+  for (int q = 0; q <= d; ++q) {
+    const V3 next = q < d ? pts[q] : rx;
+    if (!segment_visible(prev, next, kNoIe, g, s)) {
+      o.reason[k] = PCR_OCCLUDED;
+      return;
+    }
+    prev = next;
+  }
+  for (int q = 0; q < d; ++q) {
+    const size_t j = static_cast<size_t>(k) * in.stride + q;
+    store3(o.pos + 3 * j, pts[q]);
+    if (nd[q].kind == 0) {
+      store3(o.nrm + 3 * j, nd[q].n);
+      o.label[j] = nd[q].label;
+    }
+  }
+  const double total = chain_len(tx, pts, d, rx);
+  o.length[k] = total;
+  o.delay[k] = total / kSpeedOfLight;
+  o.gnorm[k] = gnorm;
+  o.reason[k] = PCR_NOT_CONVERGED;
+  o.has_path[k] = 1;
+}
+
+unsigned nb(uint64_t n, unsigned t) { return static_cast<unsigned>((n + t - 1) / t ? (n + t - 1) / t : 1); }
+
+}  // namespace
+
+void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const RefineDevIn& in,
+                   const pcr_refine_params& p, RefineDevOut& out) {
+  cudaStream_t s = ctx.stream;
+  const size_t m = in.n ? in.n : 1;
+  const size_t ms = m * in.stride;
+  out.reason.alloc(m, s);
+  out.has_path.alloc(m, s);
+  out.length.alloc(m, s);
+  out.delay.alloc(m, s);
+  out.gnorm.alloc(m, s);
+  out.iters.alloc(m, s);
+  out.pos.alloc(3 * ms, s);
+  out.nrm.alloc(3 * ms, s);
+  out.label.alloc(ms, s);
+  // positions/normals/labels start as the candidate's (kinds, ie and edge never change)
+  PCR_CUDA(cudaMemcpyAsync(out.pos.get(), in.pos, 3 * ms * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  PCR_CUDA(cudaMemcpyAsync(out.nrm.get(), in.nrm, 3 * ms * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  PCR_CUDA(cudaMemcpyAsync(out.label.get(), in.label, ms * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+  if (!in.n) return;
+  CandIn ci{in.stride, in.tx, in.rx, in.n_inter, in.kind, in.pos, in.label, in.nrm, in.edge, in.coarse_length};
+  RefOut ro{out.reason.get(), out.has_path.get(), out.pos.get(), out.nrm.get(), out.label.get(),
+            out.length.get(), out.delay.get(), out.gnorm.get(), out.iters.get()};
+  count_launch();
+  refine_kernel<<<nb(in.n, 128), 128, 0, s>>>(ci, in.n, grid.view(), scene.view(), p.delta, p.rho, p.step_size, ro);
+  PCR_LAUNCH_CHECK();
+}
+
+void api_refine_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const pcr_paths& c,
+                      const pcr_refine_params& p, pcr_outcomes** out) {
+  cudaStream_t s = ctx.stream;
+  const size_t n = c.n, st = c.stride ? c.stride : 1;
+  const size_t m = n ? n : 1, ms = m * st;
+  DBuf<double> tx(3 * m, s), rx(3 * m, s), pos(3 * ms, s), nrm(3 * ms, s), cl(m, s);
+  DBuf<uint32_t> ni(m, s), lab(ms, s), edge(ms, s);
+  DBuf<uint8_t> kind(ms, s);
+  h2d(tx.get(), c.tx_position, 3 * n, s);
+  h2d(rx.get(), c.rx_position, 3 * n, s);
+  h2d(pos.get(), c.position, 3 * n * st, s);
+  h2d(nrm.get(), c.normal, 3 * n * st, s);
+  h2d(cl.get(), c.length, n, s);
+  h2d(ni.get(), c.n_inter, n, s);
+  h2d(lab.get(), c.label, n * st, s);
+  h2d(edge.get(), c.edge_index, n * st, s);
+  h2d(kind.get(), c.kind, n * st, s);
+  for (size_t i = 0; i < n; ++i)
+    if (c.n_inter[i] > st || c.n_inter[i] > static_cast<uint32_t>(kMaxDepth))
+      throw Error(1, "refine: path longer than its stride");
+  RefineDevIn in{static_cast<uint32_t>(n), static_cast<uint32_t>(st), tx.get(), rx.get(), pos.get(), nrm.get(),
+                 cl.get(), ni.get(), lab.get(), edge.get(), kind.get()};
+  RefineDevOut ro;
+  refine_device(ctx, grid, scene, in, p, ro);
+  pcr_outcomes* o = halloc<pcr_outcomes>(1);
+  pcr_paths* pp = alloc_paths(n, static_cast<uint32_t>(st));
+  o->paths = *pp;
+  std::free(pp);
+  o->has_path = halloc<uint8_t>(n);
+  o->reason = halloc<int32_t>(n);
+  std::vector<double> rpos(3 * n * st), rnrm(3 * n * st), len(n), del(n), gn(n);
+  std::vector<uint32_t> rlab(n * st);
+  d2h(o->has_path, ro.has_path.get(), n, s);
+  d2h(o->reason, ro.reason.get(), n, s);
+  d2h(rpos.data(), ro.pos.get(), rpos.size(), s);
+  d2h(rnrm.data(), ro.nrm.get(), rnrm.size(), s);
+  d2h(rlab.data(), ro.label.get(), rlab.size(), s);
+  d2h(len.data(), ro.length.get(), n, s);
+  d2h(del.data(), ro.delay.get(), n, s);
+  d2h(gn.data(), ro.gnorm.get(), n, s);
+  PCR_CUDA(cudaStreamSynchronize(s));
+  pcr_paths& P = o->paths;
+  for (size_t i = 0; i < n; ++i) {
+    if (!o->has_path[i]) continue;
+    P.tx_id[i] = c.tx_id[i];
+    P.rx_id[i] = c.rx_id[i];
+    std::memcpy(P.tx_position + 3 * i, c.tx_position + 3 * i, 3 * sizeof(double));
+    std::memcpy(P.rx_position + 3 * i, c.rx_position + 3 * i, 3 * sizeof(double));
+    P.length[i] = len[i];
+    P.delay[i] = del[i];
+    P.converged[i] = 1;
+    P.gradient_norm[i] = gn[i];
+    P.n_inter[i] = c.n_inter[i];
+    for (uint32_t q = 0; q < c.n_inter[i]; ++q) {
+      const size_t j = i * st + q;
+      P.kind[j] = c.kind[j];
+      std::memcpy(P.position + 3 * j, &rpos[3 * j], 3 * sizeof(double));
+      P.label[j] = rlab[j];
+      std::memcpy(P.normal + 3 * j, &rnrm[3 * j], 3 * sizeof(double));
+      P.ie_index[j] = c.ie_index[j];
+      P.edge_index[j] = c.edge_index[j];
+    }
+  }
+  *out = o;
+}
+
+}  // namespace pcr

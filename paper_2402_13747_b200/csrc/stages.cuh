@@ -1,0 +1,55 @@
+// stages.cuh — device-resident stage results passed between trace.cu, refine.cu
+// and pipeline.cu.
+#pragma once
+
+#include "../../include/pcray_b200.h"
+#include "device_state.cuh"
+
+namespace pcr {
+
+// transmission_phase result for one TX (tracer.hpp:66-69), IE order kept.
+struct TxDev {
+  uint32_t n_los = 0, n_hits = 0;
+  DBuf<uint32_t> los_ie;  // IE index of each LOS candidate
+  DBuf<uint32_t> hit_ie;  // initial hits
+  DBuf<uint8_t> hit_kind;
+  DBuf<double> hit_pos, hit_nrm, hit_inc;
+};
+
+// Work counters of a propagate call (SURVEY §8d units).
+struct TraceStats {
+  uint64_t cone_traces = 0, visibility_tests = 0;
+};
+
+// Kept propagation candidates of one TX in output (DFS) order; interaction
+// arrays are row-major [n][stride].
+struct CandDev {
+  uint32_t n = 0;
+  uint32_t stride = 1;
+  DBuf<uint32_t> rx_id, n_inter, label, ie, edge;
+  DBuf<uint8_t> kind;
+  DBuf<double> rx_pos, length, pos, nrm;
+};
+
+struct RefineDevIn {
+  uint32_t n, stride;
+  const double *tx, *rx, *pos, *nrm, *coarse_length;
+  const uint32_t *n_inter, *label, *edge;
+  const uint8_t* kind;
+};
+
+struct RefineDevOut {
+  DBuf<int32_t> reason;
+  DBuf<uint8_t> has_path;
+  DBuf<double> pos, nrm, length, delay, gnorm;
+  DBuf<uint32_t> label, iters;
+};
+
+void transmission_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint32_t tx_index, TxDev& out);
+void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint32_t tx_index, const uint32_t* hit_ie,
+                      const uint8_t* hit_kind, const double* hit_pos, const double* hit_nrm, const double* hit_inc,
+                      uint32_t n_hits, const pcr_trace_params& p, CandDev& out, TraceStats& stats);
+void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const RefineDevIn& in,
+                   const pcr_refine_params& p, RefineDevOut& out);
+
+}  // namespace pcr

@@ -1,0 +1,139 @@
+// trace.cuh — stage-2 device records and the cone walk shared by the kernels.
+#pragma once
+
+#include "geom.cuh"
+
+namespace pcr {
+
+constexpr uint32_t kNoNode = 0xffffffffu;
+constexpr int kMaxDepth = 8;  // max_interactions supported by the DFS keys
+
+// One interaction of a DFS path (tracer.hpp:31-38 Interaction) plus the links
+// the wavefront needs: the parent interaction, the Keller-fan index of the
+// parent ray that produced this reception, and the number of child rays.
+struct Node {
+  double pos[3];
+  double nrm[3];  // reflection: surface normal at the hit; diffraction: edge normal_a
+  double inc[3];  // incoming direction at this interaction
+  uint32_t parent;
+  uint32_t parent_j;
+  uint32_t ie, label, edge;
+  uint32_t task;  // index of the initial hit this path descends from
+  uint32_t n_children;
+  uint8_t kind, depth, dc, pad;
+};
+
+// A materialised conical ray (tracer.hpp:40-47). Separation planes all pass
+// through the ray origin (tracer.cpp:265, 306-307), so only normals are kept.
+struct Ray {
+  V3 o, d;
+  double apex;
+  V3 pn[2];
+  uint32_t node, j;
+  uint32_t origin_ie, origin_label;
+  uint8_t n_planes, depth, dc, alive;
+};
+
+struct Cand {
+  uint32_t node, j, rx_ie, pad;
+};
+
+// Visibility work item: ray r may receive IE i.
+struct Task {
+  uint32_t ray, ie;
+};
+
+// passes_separation_planes (tracer.cpp:99-104)
+__device__ __forceinline__ bool passes_planes(const Ray& r, const V3& q) {
+  for (int k = 0; k < r.n_planes; ++k)
+    if (dot(q - r.o, r.pn[k]) < 0.0) return false;
+  return true;
+}
+
+// voxel_cone_trace walk (tracer.cpp:313-398). on_eval(cell) sees every newly
+// evaluated in-bounds cell (TraceDebug::evaluated); on_ie(i) every IE that passes
+// the self-exclusion, cone, plane and coincidence tests and so reaches
+// segment_visible. The `evaluated` byte array (tracer.cpp:329) is replaced by an
+// exact ring of the last evaluating voxels: voxel coordinates are monotone along
+// the walk (DDA steps and forward re-inits), so a cell of N(v) was evaluated iff
+// it lies in N(u) for an earlier evaluating voxel u within Chebyshev distance 2
+// of v, and those u are a suffix of at most 6 voxels.
+template <typename OnEval, typename OnIE>
+__device__ __forceinline__ void cone_walk(const GridView& g, const Ray& r, OnEval on_eval, OnIE on_ie) {
+  if (g.n_ies == 0) return;
+  const double half_angle = 0.5 * r.apex;
+  const double exempt_radius = 2.0 * g.sub_radius;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  int ring[8][3];
+  int ring_n = 0;
+  Walker w;
+  w.init(g, r.o, r.d, 0.0, inf);
+  while (w.active) {
+    const int4 here = g.cells[linear_index(g, w.v[0], w.v[1], w.v[2])];
+    const int march = here.z;
+    if (here.x != here.y || march <= 1) {
+      for (int oz = -1; oz <= 1; ++oz) {
+        for (int oy = -1; oy <= 1; ++oy) {
+          for (int ox = -1; ox <= 1; ++ox) {
+            const int nx = w.v[0] + ox, ny = w.v[1] + oy, nz = w.v[2] + oz;
+            if (!in_bounds(g, nx, ny, nz)) continue;
+            bool seen = false;
+            for (int k = 0; k < ring_n; ++k) {
+              if (abs(nx - ring[k][0]) <= 1 && abs(ny - ring[k][1]) <= 1 && abs(nz - ring[k][2]) <= 1) {
+                seen = true;
+                break;
+              }
+            }
+            if (seen) continue;
+            const uint32_t ni = linear_index(g, nx, ny, nz);
+            on_eval(ni);
+            const int4 cell = g.cells[ni];
+            if (cell.x == cell.y) continue;
+            if (!cone_intersects_sphere(r.o, r.d, half_angle, voxel_center(g, nx, ny, nz), g.voxel_radius)) continue;
+            for (uint32_t i = static_cast<uint32_t>(cell.x); i < static_cast<uint32_t>(cell.y); ++i) {
+              if (i == r.origin_ie) continue;
+              const double4 sc4 = g.ie_sc[i];
+              const V3 sc = ld3(sc4);
+              if (r.origin_ie != kNoIe && g.ie_label[i] == r.origin_label && norm(sc - r.o) <= exempt_radius)
+                continue;
+              if (!cone_intersects_sphere(r.o, r.d, half_angle, sc, sc4.w)) continue;
+              const V3 rp = ld3(g.ie_rp[i]);
+              if (!passes_planes(r, rp)) continue;
+              if (norm(rp - r.o) < kTiny) continue;
+              on_ie(i);
+            }
+          }
+        }
+      }
+      // keep only earlier evaluating voxels still within Chebyshev distance 2
+      int m = 0;
+      for (int k = 0; k < ring_n; ++k) {
+        if (abs(w.v[0] - ring[k][0]) <= 2 && abs(w.v[1] - ring[k][1]) <= 2 && abs(w.v[2] - ring[k][2]) <= 2) {
+          ring[m][0] = ring[k][0];
+          ring[m][1] = ring[k][1];
+          ring[m][2] = ring[k][2];
+          ++m;
+        }
+      }
+      if (m == 8) {  // cannot happen (<= 6 by monotonicity); keep the newest 7
+        for (int k = 0; k < 7; ++k) {
+          ring[k][0] = ring[k + 1][0];
+          ring[k][1] = ring[k + 1][1];
+          ring[k][2] = ring[k + 1][2];
+        }
+        m = 7;
+      }
+      ring[m][0] = w.v[0];
+      ring[m][1] = w.v[1];
+      ring[m][2] = w.v[2];
+      ring_n = m + 1;
+    }
+    if (march >= 2) {
+      w.init(g, r.o, r.d, w.t_entry + static_cast<double>(march - 1) * g.voxel_size, inf);
+    } else {
+      w.advance(g);
+    }
+  }
+}
+
+}  // namespace pcr

@@ -1,0 +1,283 @@
+"""Python mirror of the reference's C++ API (namespace ``pcray``) over the B200 C ABI.
+
+Each function forwards to one ``pcr_*`` entry point of libpcray_b200.so (see
+include/pcray_b200.h) and keeps the reference's name, argument meaning, output
+order and error text. There is no CPU path: if the CUDA library is missing or no
+GPU is visible, calls raise ``PcrError`` — nothing falls back to the oracle.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import abi
+from .abi import (RunConfig, Scene, TraceParams, RefineParams, VoxelParams, default_run_config, refine_params,
+                  trace_params, voxel_params)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpcray_b200.so")
+
+_lib = None
+
+
+class PcrError(RuntimeError):
+    """std::runtime_error of the reference; .code is the pcr_status."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+def lib():
+    """Load the in-tree CUDA library (fails loudly when it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise PcrError(2, f"CUDA library not built: {LIB_PATH} (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        vp, pp = C.c_void_p, C.POINTER
+        L.pcr_abi_version.restype = C.c_int
+        L.pcr_create.argtypes = [C.c_int, pp(vp)]
+        L.pcr_destroy.argtypes = [vp]
+        L.pcr_last_error.restype = C.c_char_p
+        L.pcr_last_error.argtypes = [vp]
+        L.pcr_kernel_launches.restype = C.c_uint64
+        L.pcr_scene_upload.argtypes = [vp, pp(abi.SceneDesc), pp(vp)]
+        L.pcr_scene_free.argtypes = [vp]
+        L.pcr_build_grid.argtypes = [vp, vp, pp(abi.VoxelParams), pp(vp)]
+        L.pcr_grid_upload.argtypes = [vp, pp(abi.GridHost), pp(vp)]
+        L.pcr_compute_march_distances.argtypes = [vp, vp]
+        L.pcr_grid_download.argtypes = [vp, vp, pp(pp(abi.GridHost))]
+        L.pcr_grid_free.argtypes = [vp]
+        L.pcr_free_grid_host.argtypes = [pp(abi.GridHost)]
+        L.pcr_transmission_phase.argtypes = [vp, vp, vp, C.c_uint32, pp(abi.TraceParams), pp(pp(abi.Paths)),
+                                             pp(pp(abi.InitialHits))]
+        L.pcr_propagate.argtypes = [vp, vp, vp, C.c_uint32, pp(abi.InitialHits), pp(abi.TraceParams),
+                                    pp(pp(abi.Paths))]
+        L.pcr_cone_trace_batch.argtypes = [vp, vp, vp, pp(abi.RayDesc), C.c_uint64, C.c_int,
+                                           pp(pp(abi.Receptions))]
+        L.pcr_segment_visible_batch.argtypes = [vp, vp, vp, pp(C.c_double), pp(C.c_double), pp(C.c_uint32),
+                                                C.c_uint64, pp(C.c_uint8)]
+        L.pcr_refine_batch.argtypes = [vp, vp, vp, pp(abi.Paths), pp(abi.RefineParams), pp(pp(abi.Outcomes))]
+        L.pcr_run_pipeline_on_scene.argtypes = [vp, pp(abi.SceneDesc), pp(abi.RunConfig), pp(pp(abi.Summary))]
+        L.pcr_config_hash.restype = C.c_uint64
+        L.pcr_config_hash.argtypes = [pp(abi.RunConfig)]
+        L.pcr_run_config_defaults.argtypes = [pp(abi.RunConfig)]
+        for name, t in [("pcr_free_paths", abi.Paths), ("pcr_free_initial_hits", abi.InitialHits),
+                        ("pcr_free_outcomes", abi.Outcomes), ("pcr_free_summary", abi.Summary),
+                        ("pcr_free_receptions", abi.Receptions)]:
+            getattr(L, name).argtypes = [pp(t)]
+        if L.pcr_abi_version() != 1:
+            raise PcrError(1, "ABI version mismatch")
+        _lib = L
+    return _lib
+
+
+EXPORTED_SYMBOLS = [
+    "pcr_abi_version", "pcr_create", "pcr_destroy", "pcr_last_error", "pcr_scene_upload", "pcr_scene_free",
+    "pcr_build_grid", "pcr_grid_upload", "pcr_compute_march_distances", "pcr_grid_download", "pcr_grid_free",
+    "pcr_free_grid_host", "pcr_transmission_phase", "pcr_propagate", "pcr_cone_trace_batch",
+    "pcr_segment_visible_batch", "pcr_refine_batch", "pcr_run_pipeline_on_scene", "pcr_config_hash",
+    "pcr_run_config_defaults", "pcr_free_paths", "pcr_free_initial_hits", "pcr_free_outcomes",
+    "pcr_free_summary", "pcr_free_receptions",
+]
+
+
+class Context:
+    """One device context (pcr_create). Calls on one context are serialised."""
+
+    _default = None
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        rc = lib().pcr_create(device, C.byref(h))
+        if rc != 0:
+            raise PcrError(rc, f"pcr_create(device={device}) failed (no CUDA device?)")
+        self.handle = h
+
+    @classmethod
+    def default(cls) -> "Context":
+        if cls._default is None:
+            cls._default = Context(int(os.environ.get("PCR_DEVICE", "0")))
+        return cls._default
+
+    def check(self, rc: int):
+        if rc != 0:
+            raise PcrError(rc, lib().pcr_last_error(self.handle).decode())
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.pcr_destroy(self.handle)
+            self.handle = None
+
+
+def kernel_launches() -> int:
+    """Number of library kernel launches so far in this process."""
+    return int(lib().pcr_kernel_launches())
+
+
+class DeviceScene:
+    """Scene resident on the GPU (pcr_scene_upload)."""
+
+    def __init__(self, scene: Scene, ctx: Context | None = None):
+        self.ctx = ctx or Context.default()
+        self.keep = abi.SceneKeepAlive(scene)
+        self.scene = self.keep.scene
+        h = C.c_void_p()
+        self.ctx.check(lib().pcr_scene_upload(self.ctx.handle, C.byref(self.keep.desc), C.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.pcr_scene_free(self.handle)
+            self.handle = None
+
+
+class DeviceGrid:
+    """VoxelGrid resident on the GPU; .to_dict() is the host VoxelGrid mirror."""
+
+    def __init__(self, handle, ctx: Context):
+        self.handle = handle
+        self.ctx = ctx
+
+    @classmethod
+    def from_dict(cls, g: dict, ctx: Context | None = None) -> "DeviceGrid":
+        ctx = ctx or Context.default()
+        keep = abi.GridKeepAlive(g)
+        h = C.c_void_p()
+        ctx.check(lib().pcr_grid_upload(ctx.handle, C.byref(keep.host), C.byref(h)))
+        return cls(h, ctx)
+
+    def to_dict(self) -> dict:
+        out = C.POINTER(abi.GridHost)()
+        self.ctx.check(lib().pcr_grid_download(self.ctx.handle, self.handle, C.byref(out)))
+        try:
+            return abi.grid_to_dict(out.contents)
+        finally:
+            lib().pcr_free_grid_host(out)
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.pcr_grid_free(self.handle)
+            self.handle = None
+
+
+def _as_dev_scene(scene) -> DeviceScene:
+    return scene if isinstance(scene, DeviceScene) else DeviceScene(scene)
+
+
+# ---- stage 1 -----------------------------------------------------------------------------------
+def build_grid(scene, params: VoxelParams | None = None) -> DeviceGrid:
+    """pcray::build_grid (voxel_grid.hpp:99)."""
+    ds = _as_dev_scene(scene)
+    params = params or voxel_params()
+    h = C.c_void_p()
+    ds.ctx.check(lib().pcr_build_grid(ds.ctx.handle, ds.handle, C.byref(params), C.byref(h)))
+    return DeviceGrid(h, ds.ctx)
+
+
+def compute_march_distances(grid: DeviceGrid) -> None:
+    """pcray::compute_march_distances (voxel_grid.hpp:103), in place."""
+    grid.ctx.check(lib().pcr_compute_march_distances(grid.ctx.handle, grid.handle))
+
+
+# ---- stage 2 -----------------------------------------------------------------------------------
+def transmission_phase(tx_index: int, grid: DeviceGrid, scene: DeviceScene, params: TraceParams | None = None):
+    """pcray::transmission_phase (tracer.hpp:94-95) -> (los_paths, initial_hits)."""
+    params = params or trace_params()
+    los = C.POINTER(abi.Paths)()
+    hits = C.POINTER(abi.InitialHits)()
+    grid.ctx.check(lib().pcr_transmission_phase(grid.ctx.handle, grid.handle, scene.handle, tx_index,
+                                                C.byref(params), C.byref(los), C.byref(hits)))
+    try:
+        return abi.paths_to_dict(los.contents), abi.hits_to_dict(hits.contents)
+    finally:
+        lib().pcr_free_paths(los)
+        lib().pcr_free_initial_hits(hits)
+
+
+def propagate(tx_index: int, hits: dict, grid: DeviceGrid, scene: DeviceScene, params: TraceParams | None = None):
+    """pcray::propagate (tracer.hpp:122-124) -> candidates in (task, DFS) order after kappa."""
+    params = params or trace_params()
+    keep = abi.HitsKeepAlive(hits)
+    out = C.POINTER(abi.Paths)()
+    grid.ctx.check(lib().pcr_propagate(grid.ctx.handle, grid.handle, scene.handle, tx_index, C.byref(keep.hits),
+                                       C.byref(params), C.byref(out)))
+    try:
+        return abi.paths_to_dict(out.contents)
+    finally:
+        lib().pcr_free_paths(out)
+
+
+def make_ray(origin, direction, apex_angle, planes=(), origin_ie=abi.NO_IE, origin_label=0) -> abi.RayDesc:
+    r = abi.RayDesc()
+    r.origin[:] = [float(x) for x in origin]
+    r.direction[:] = [float(x) for x in direction]
+    r.apex_angle = float(apex_angle)
+    r.n_planes = len(planes)
+    for k, (p, n) in enumerate(planes):
+        r.plane_point[k][:] = [float(x) for x in p]
+        r.plane_normal[k][:] = [float(x) for x in n]
+    r.origin_ie = origin_ie
+    r.origin_label = origin_label
+    return r
+
+
+def voxel_cone_trace(rays, grid: DeviceGrid, scene: DeviceScene, want_debug: bool = False) -> dict:
+    """pcray::voxel_cone_trace (tracer.hpp:118-120) over a batch of rays (CSR receptions)."""
+    arr = (abi.RayDesc * max(1, len(rays)))(*rays)
+    out = C.POINTER(abi.Receptions)()
+    grid.ctx.check(lib().pcr_cone_trace_batch(grid.ctx.handle, grid.handle, scene.handle, arr, len(rays),
+                                              int(want_debug), C.byref(out)))
+    try:
+        return abi.receptions_to_dict(out.contents)
+    finally:
+        lib().pcr_free_receptions(out)
+
+
+def segment_visible(origin, target, target_ie, grid: DeviceGrid, scene: DeviceScene) -> np.ndarray:
+    """pcray::segment_visible (tracer.hpp:88-89), batched."""
+    o = np.ascontiguousarray(origin, dtype=np.float64).reshape(-1, 3)
+    t = np.ascontiguousarray(target, dtype=np.float64).reshape(-1, 3)
+    ti = np.ascontiguousarray(np.broadcast_to(np.asarray(target_ie, dtype=np.uint32), (len(o),)))
+    out = np.zeros(len(o), dtype=np.uint8)
+    dp = C.POINTER(C.c_double)
+    grid.ctx.check(lib().pcr_segment_visible_batch(grid.ctx.handle, grid.handle, scene.handle, o.ctypes.data_as(dp),
+                                                   t.ctypes.data_as(dp), ti.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                                   len(o), out.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return out
+
+
+# ---- stage 3 -----------------------------------------------------------------------------------
+def refine_paths(candidates: dict, grid: DeviceGrid, scene: DeviceScene, params: RefineParams | None = None) -> dict:
+    """pcray::refine_path (refine.hpp:77-78) for every candidate (LOS rows pass through)."""
+    params = params or refine_params()
+    keep = abi.PathsKeepAlive(candidates)
+    out = C.POINTER(abi.Outcomes)()
+    grid.ctx.check(lib().pcr_refine_batch(grid.ctx.handle, grid.handle, scene.handle, C.byref(keep.paths),
+                                          C.byref(params), C.byref(out)))
+    try:
+        return abi.outcomes_to_dict(out.contents)
+    finally:
+        lib().pcr_free_outcomes(out)
+
+
+# ---- pipeline ----------------------------------------------------------------------------------
+def run_pipeline_on_scene(scene: Scene, config: RunConfig | None = None, ctx: Context | None = None) -> dict:
+    """pcray::run_pipeline_on_scene (pipeline.hpp:61) -> RunSummary as a dict."""
+    ctx = ctx or Context.default()
+    config = config or default_run_config()
+    keep = abi.SceneKeepAlive(scene)
+    out = C.POINTER(abi.Summary)()
+    ctx.check(lib().pcr_run_pipeline_on_scene(ctx.handle, C.byref(keep.desc), C.byref(config), C.byref(out)))
+    try:
+        return abi.summary_to_dict(out.contents)
+    finally:
+        lib().pcr_free_summary(out)
+
+
+def config_hash(config: RunConfig) -> int:
+    """pcray::config_hash (pipeline.hpp:39)."""
+    return int(lib().pcr_config_hash(C.byref(config)))
