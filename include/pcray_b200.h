@@ -196,6 +196,10 @@ typedef struct pcr_summary {
   uint64_t cone_traces;       /* voxel_cone_trace invocations (= dfs_trace calls) */
   uint64_t visibility_tests;  /* segment_visible invocations */
   uint64_t refine_iterations; /* refinement iterations summed over candidates */
+  uint64_t refine_trials;     /* backtracking trial path lengths evaluated */
+  uint64_t refine_marches;    /* march_segment / projection calls inside reproject */
+  uint64_t walk_cells;        /* cells evaluated by cone walks (neighbourhood scans) */
+  uint64_t walk_ies;          /* IE records tested by cone walks */
 } pcr_summary;
 
 /* A conical ray (tracer.hpp:40-47) for the batch primitives; planes are given
@@ -237,6 +241,8 @@ void pcr_destroy(pcr_ctx* ctx);
 const char* pcr_last_error(const pcr_ctx* ctx);
 /* number of library kernel launches issued by this process (bench accounting) */
 uint64_t pcr_kernel_launches(void);
+/* bytes copied host->device and device->host by the library in this process */
+void pcr_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
 
 /* ---- scene / grid residency ----------------------------------------------- */
 int pcr_scene_upload(pcr_ctx* ctx, const pcr_scene_desc* desc, pcr_scene** out);
@@ -280,6 +286,23 @@ int pcr_refine_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene,
 /* run_pipeline_on_scene (pipeline.hpp:61; pipeline.cpp:99-212) */
 int pcr_run_pipeline_on_scene(pcr_ctx* ctx, const pcr_scene_desc* scene,
                               const pcr_run_config* config, pcr_summary** out);
+/* The same pipeline over a scene already resident on the device (pcr_scene_upload);
+ * the "validate" stage then covers only the device-side checks. */
+int pcr_run_pipeline_device(pcr_ctx* ctx, const pcr_scene* scene, const pcr_run_config* config,
+                            pcr_summary** out);
+
+/* ---- instrumentation (no reference counterpart) ------------------------------------ */
+/* cudaStream_t the context launches on, as an opaque pointer (for caller-side events) */
+void* pcr_stream(pcr_ctx* ctx);
+/* per-kernel CUDA-event timing of subsequent calls: on != 0 enables, 0 disables */
+int pcr_set_profiling(pcr_ctx* ctx, int on);
+/* accumulated per-kernel totals since the last reset; returns the number of entries
+ * (at most cap); names are NUL-terminated, 32 bytes each. reset != 0 clears them. */
+int pcr_kernel_times(pcr_ctx* ctx, char (*names)[32], double* ms, uint64_t* launches, int cap, int reset);
+
+/* measured non-FMA FP64 throughput of this device (TFLOP/s), the refinement roofline */
+int pcr_fp64_probe(pcr_ctx* ctx, double* tflops);
+
 /* config_hash (pipeline.hpp:39; pipeline.cpp:89-97) */
 uint64_t pcr_config_hash(const pcr_run_config* config);
 void pcr_run_config_defaults(pcr_run_config* config);

@@ -20,7 +20,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_ref", "libpcray_ref.so")
 REFERENCE_SRC = "/root/reference/proj"
 
-_lib = None
+COUNT_LIB_PATH = os.path.join(HERE, "_ref", "libpcray_ref_count.so")
+
+_lib = None          # the library the module functions currently use
+_libs = {}           # path -> loaded CDLL
 
 
 def build(force: bool = False) -> None:
@@ -33,12 +36,44 @@ def available() -> bool:
     return os.path.exists(LIB_PATH)
 
 
+class counting:
+    """Context manager: route calls to the counting build (voxel_cone_trace /
+    segment_visible entry counters; slower, never timed). Objects created inside
+    must be used and freed inside."""
+
+    def __enter__(self):
+        global _lib
+        self.prev = lib()
+        _lib = _load(COUNT_LIB_PATH)
+        _lib.pcrref_counters.argtypes = [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_int]
+        return self
+
+    def read(self, reset=True):
+        a, b = C.c_uint64(), C.c_uint64()
+        _lib.pcrref_counters(C.byref(a), C.byref(b), int(reset))
+        return int(a.value), int(b.value)
+
+    def __exit__(self, *exc):
+        global _lib
+        import gc
+
+        gc.collect()
+        _lib = self.prev
+        return False
+
+
 def lib():
     global _lib
     if _lib is None:
-        if not available():
+        _lib = _load(LIB_PATH)
+    return _lib
+
+
+def _load(path):
+    if path not in _libs:
+        if not os.path.exists(path):
             build()
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         vp = C.c_void_p
         pp = C.POINTER
         L.pcrref_last_error.restype = C.c_char_p
@@ -79,8 +114,8 @@ def lib():
                                                  pp(C.c_double), pp(C.c_double), pp(C.c_uint32)]
         L.pcrref_image_method_paths.argtypes = [pp(C.c_double), C.c_uint32, pp(C.c_double), pp(C.c_double),
                                                 C.c_int, pp(pp(abi.Paths))]
-        _lib = L
-    return _lib
+        _libs[path] = L
+    return _libs[path]
 
 
 class RefError(RuntimeError):
@@ -100,11 +135,12 @@ class RefScene:
     def __init__(self, scene: abi.Scene):
         self.keep = abi.SceneKeepAlive(scene)
         self.scene = self.keep.scene
-        self.handle = lib().pcrref_scene_create(C.byref(self.keep.desc))
+        self.L = lib()
+        self.handle = self.L.pcrref_scene_create(C.byref(self.keep.desc))
 
     def __del__(self):
-        if getattr(self, "handle", None) and _lib is not None:
-            _lib.pcrref_scene_free(self.handle)
+        if getattr(self, "handle", None):
+            self.L.pcrref_scene_free(self.handle)
             self.handle = None
 
     def validate(self):
@@ -116,6 +152,7 @@ class RefScene:
 class RefGrid:
     def __init__(self, handle):
         self.handle = handle
+        self.L = lib()
 
     @classmethod
     def build(cls, scene: RefScene, params: abi.VoxelParams | None = None) -> "RefGrid":
@@ -143,8 +180,8 @@ class RefGrid:
             lib().pcrref_free_grid_host(out)
 
     def __del__(self):
-        if getattr(self, "handle", None) and _lib is not None:
-            _lib.pcrref_grid_free(self.handle)
+        if getattr(self, "handle", None):
+            self.L.pcrref_grid_free(self.handle)
             self.handle = None
 
 

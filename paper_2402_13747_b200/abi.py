@@ -99,6 +99,8 @@ class Summary(C.Structure):
         ("timing_stage", (C.c_char * 16) * MAX_STAGES), ("timing_seconds", C.c_double * MAX_STAGES),
         ("hash", C.c_uint64), ("paths", Paths), ("transmission_rays", C.c_uint64),
         ("cone_traces", C.c_uint64), ("visibility_tests", C.c_uint64), ("refine_iterations", C.c_uint64),
+        ("refine_trials", C.c_uint64), ("refine_marches", C.c_uint64), ("walk_cells", C.c_uint64),
+        ("walk_ies", C.c_uint64),
     ]
 
 
@@ -298,6 +300,8 @@ def summary_to_dict(s: Summary) -> dict:
         "hash": int(s.hash), "paths": paths_to_dict(s.paths),
         "transmission_rays": int(s.transmission_rays), "cone_traces": int(s.cone_traces),
         "visibility_tests": int(s.visibility_tests), "refine_iterations": int(s.refine_iterations),
+        "refine_trials": int(s.refine_trials), "refine_marches": int(s.refine_marches),
+        "walk_cells": int(s.walk_cells), "walk_ies": int(s.walk_ies),
     }
 
 

@@ -6,18 +6,9 @@
 #include <vector>
 
 #include "device_state.cuh"
+#include "handles.cuh"
 #include "host_alloc.hpp"
 #include "pipeline.hpp"
-
-struct pcr_ctx {
-  pcr::Ctx c;
-};
-struct pcr_scene {
-  pcr::SceneDev s;
-};
-struct pcr_grid {
-  pcr::GridDev g;
-};
 
 namespace {
 
@@ -92,38 +83,17 @@ const char* pcr_last_error(const pcr_ctx* ctx) { return ctx ? ctx->c.last_error.
 
 uint64_t pcr_kernel_launches(void) { return pcr::g_launch_count; }
 
+void pcr_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
+  if (h2d) *h2d = pcr::g_h2d_bytes;
+  if (d2h) *d2h = pcr::g_d2h_bytes;
+}
+
 int pcr_scene_upload(pcr_ctx* ctx, const pcr_scene_desc* d, pcr_scene** out) {
   return guarded(ctx, [&] {
     if (!d || !out) throw pcr::Error(PCR_ERR_INVALID, "null argument");
-    cudaStream_t s = ctx->c.stream;
     auto* sc = new pcr_scene();
     try {
-      pcr::SceneDev& S = sc->s;
-      S.n_points = d->n_points;
-      const size_t n = d->n_points;
-      S.pos.alloc(3 * n + 3, s);
-      S.nrm.alloc(3 * n + 3, s);
-      S.label.alloc(n + 1, s);
-      pcr::h2d(S.pos.get(), d->point_position, 3 * n, s);
-      pcr::h2d(S.nrm.get(), d->point_normal, 3 * n, s);
-      pcr::h2d(S.label.get(), d->point_label, n, s);
-      S.n_edges = d->n_edges;
-      S.h_edges.assign(d->edge_geometry, d->edge_geometry + 12ull * d->n_edges);
-      S.h_edge_label.assign(d->edge_label, d->edge_label + d->n_edges);
-      S.edges.alloc(12ull * d->n_edges + 12, s);
-      S.edge_label.alloc(d->n_edges + 1ull, s);
-      pcr::h2d(S.edges.get(), S.h_edges.data(), S.h_edges.size(), s);
-      pcr::h2d(S.edge_label.get(), S.h_edge_label.data(), S.h_edge_label.size(), s);
-      S.h_tx.assign(d->tx_position, d->tx_position + 3ull * d->n_tx);
-      S.h_tx_id.assign(d->tx_id, d->tx_id + d->n_tx);
-      S.h_rx.assign(d->rx_position, d->rx_position + 3ull * d->n_rx);
-      S.h_rx_id.assign(d->rx_id, d->rx_id + d->n_rx);
-      S.rx_pos.alloc(3ull * d->n_rx + 3, s);
-      S.rx_id.alloc(d->n_rx + 1ull, s);
-      pcr::h2d(S.rx_pos.get(), S.h_rx.data(), S.h_rx.size(), s);
-      pcr::h2d(S.rx_id.get(), S.h_rx_id.data(), S.h_rx_id.size(), s);
-      S.carrier_frequency_hz = d->carrier_frequency_hz;
-      PCR_CUDA(cudaStreamSynchronize(s));
+      pcr::upload_scene(ctx->c, *d, sc->s);
     } catch (...) {
       delete sc;
       throw;
@@ -366,6 +336,39 @@ int pcr_run_pipeline_on_scene(pcr_ctx* ctx, const pcr_scene_desc* scene, const p
     if (!scene || !config || !out) throw pcr::Error(PCR_ERR_INVALID, "null argument");
     pcr::api_run_pipeline_on_scene(ctx->c, *scene, *config, out);
   });
+}
+
+int pcr_run_pipeline_device(pcr_ctx* ctx, const pcr_scene* scene, const pcr_run_config* config,
+                            pcr_summary** out) {
+  return guarded(ctx, [&] {
+    if (!scene || !config || !out) throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    pcr::api_run_pipeline_device(ctx->c, scene->s, *config, out);
+  });
+}
+
+void* pcr_stream(pcr_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c.stream) : nullptr; }
+
+int pcr_set_profiling(pcr_ctx* ctx, int on) {
+  return guarded(ctx, [&] {
+    ctx->c.resolve_timers();
+    ctx->c.profiling = on != 0;
+  });
+}
+
+int pcr_kernel_times(pcr_ctx* ctx, char (*names)[32], double* ms, uint64_t* launches, int cap, int reset) {
+  int n = 0;
+  const int rc = guarded(ctx, [&] {
+    ctx->c.resolve_timers();
+    for (const auto& kv : ctx->c.totals) {
+      if (n >= cap) break;
+      std::snprintf(names[n], 32, "%s", kv.first.c_str());
+      ms[n] = kv.second.ms;
+      launches[n] = kv.second.launches;
+      ++n;
+    }
+    if (reset) ctx->c.totals.clear();
+  });
+  return rc == PCR_OK ? n : -rc;
 }
 
 uint64_t pcr_config_hash(const pcr_run_config* c) { return pcr::config_hash(*c); }

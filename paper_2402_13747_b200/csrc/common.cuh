@@ -87,18 +87,24 @@ inline unsigned blocks_for(uint64_t n, unsigned threads, unsigned cap = 148u * 6
   return static_cast<unsigned>(b < cap ? b : cap);
 }
 
+// Launch and transfer accounting: every kernel launch and host<->device copy of the
+// library goes through these counters so bench.py can report them per timed step.
+extern uint64_t g_launch_count, g_h2d_bytes, g_d2h_bytes;
+inline void count_launch() { ++g_launch_count; }
+
 template <typename T>
 void d2h(T* dst, const T* src, size_t n, cudaStream_t s) {
-  if (n) PCR_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  if (n) {
+    PCR_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    g_d2h_bytes += n * sizeof(T);
+  }
 }
 template <typename T>
 void h2d(T* dst, const T* src, size_t n, cudaStream_t s) {
-  if (n) PCR_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  if (n) {
+    PCR_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    g_h2d_bytes += n * sizeof(T);
+  }
 }
-
-// Launch accounting: every kernel launch of the library goes through this
-// counter so bench.py can report how many of our kernels ran in a timed region.
-extern uint64_t g_launch_count;
-inline void count_launch() { ++g_launch_count; }
 
 }  // namespace pcr

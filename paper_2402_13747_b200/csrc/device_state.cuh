@@ -125,7 +125,62 @@ struct Ctx {
   int fan_n = 0;
   DBuf<double> fan_table;  // n*6: cos phi, sin phi, sin(phi+dphi/2), cos(phi+dphi/2), sin(phi-dphi/2), cos(phi-dphi/2)
   int sm_count = 148;
+  // per-kernel CUDA-event timing (pcr_set_profiling); resolved lazily
+  bool profiling = false;
+  struct Pending {
+    const char* name;
+    cudaEvent_t a, b;
+    double units;  // algorithmic work of the launch (bytes or flops, kernel-specific)
+  };
+  std::vector<Pending> pending;
+  struct Total {
+    double ms = 0, units = 0;
+    uint64_t launches = 0;
+  };
+  std::vector<std::pair<std::string, Total>> totals;
+  void resolve_timers();
 };
+
+// Scoped timer around one kernel launch on ctx.stream (no-op unless profiling).
+struct KTimer {
+  Ctx& c;
+  const char* name;
+  cudaEvent_t a = nullptr, b = nullptr;
+  double units;
+  KTimer(Ctx& ctx, const char* n, double u = 0) : c(ctx), name(n), units(u) {
+    if (!c.profiling) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, c.stream);
+  }
+  ~KTimer() {
+    if (!c.profiling) return;
+    cudaEventRecord(b, c.stream);
+    c.pending.push_back({name, a, b, units});
+  }
+};
+
+inline void Ctx::resolve_timers() {
+  if (pending.empty()) return;
+  cudaStreamSynchronize(stream);
+  for (auto& p : pending) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+    Total* t = nullptr;
+    for (auto& kv : totals)
+      if (kv.first == p.name) t = &kv.second;
+    if (!t) {
+      totals.emplace_back(p.name, Total{});
+      t = &totals.back().second;
+    }
+    t->ms += ms;
+    t->units += p.units;
+    t->launches += 1;
+  }
+  pending.clear();
+}
 
 // stage 1 (voxelize.cu)
 void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int division_factor,

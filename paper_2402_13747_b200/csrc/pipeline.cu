@@ -37,60 +37,96 @@ uint64_t fnv1a(const char* s) {
   return h;
 }
 
-// ---- validate_scene -------------------------------------------------------------------------
+// ---- validate_scene (scene.cpp:31-91) ---------------------------------------------------------
+// The O(N) point checks run on the device (SURVEY §8f "next" #1): the first offending
+// point index (atomicMin) and, per edge, whether any point carries its label. Edges and
+// radios are few and are checked on the host in the reference's report order.
 struct Violation {
   std::string rule, detail;
   size_t index;
 };
 
-bool finite3(const double* p) { return std::isfinite(p[0]) && std::isfinite(p[1]) && std::isfinite(p[2]); }
-double norm3(const double* p) { return std::sqrt((p[0] * p[0] + p[1] * p[1]) + p[2] * p[2]); }
+__global__ void validate_points_kernel(const double* __restrict__ pos, const double* __restrict__ nrm,
+                                       const uint32_t* __restrict__ label, uint64_t n,
+                                       const uint32_t* __restrict__ edge_label, uint32_t n_edges,
+                                       unsigned long long* __restrict__ first_bad, uint32_t* __restrict__ label_hit) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const V3 p = load3(pos + 3 * i), q = load3(nrm + 3 * i);
+    const bool finite = isfinite(p.x) && isfinite(p.y) && isfinite(p.z);
+    const double nn = norm(q);
+    if (!finite || fabs(nn - 1.0) > 1e-6) atomicMin(first_bad, static_cast<unsigned long long>(i));
+    const uint32_t l = label[i];
+    for (uint32_t e = 0; e < n_edges; ++e)
+      if (edge_label[e] == l && !label_hit[e]) label_hit[e] = 1;
+  }
+}
 
-// Returns the first violation in the reference's report order, if any.
-bool first_violation(const pcr_scene_desc& d, Violation& v) {
+bool first_violation_device(Ctx& ctx, const SceneDev& S, Violation& v) {
+  cudaStream_t s = ctx.stream;
+  DBuf<unsigned long long> first(1, s);
+  DBuf<uint32_t> hit(S.n_edges + 1ull, s);
+  const unsigned long long none = ~0ull;
+  h2d(first.get(), &none, 1, s);
+  PCR_CUDA(cudaMemsetAsync(hit.get(), 0, (S.n_edges + 1ull) * sizeof(uint32_t), s));
+  if (S.n_points) {
+    count_launch();
+    KTimer kt(ctx, "validate");
+    validate_points_kernel<<<blocks_for(S.n_points, 256, 148u * 8u), 256, 0, s>>>(
+        S.pos.get(), S.nrm.get(), S.label.get(), S.n_points, S.edge_label.get(), S.n_edges, first.get(), hit.get());
+    PCR_LAUNCH_CHECK();
+  }
+  unsigned long long fb = none;
+  std::vector<uint32_t> lh(S.n_edges + 1ull);
+  d2h(&fb, first.get(), 1, s);
+  d2h(lh.data(), hit.get(), lh.size(), s);
+  PCR_CUDA(cudaStreamSynchronize(s));
   std::vector<Violation> out;
   auto add = [&](const std::string& rule, size_t i, const std::string& detail) {
     if (out.empty()) out.push_back({rule, detail, i});
   };
-  const bool need_labels = d.n_edges > 0;
-  std::unordered_set<uint32_t> labels;
-  for (uint64_t i = 0; i < d.n_points; ++i) {
-    if (!finite3(d.point_position + 3 * i)) add("point_position_finite", i, "non-finite position");
-    const double nn = norm3(d.point_normal + 3 * i);
-    if (std::abs(nn - 1.0) > 1e-6) add("point_normal_unit", i, "normal length " + std::to_string(nn));
-    if (need_labels) labels.insert(d.point_label[i]);
-    if (!out.empty() && !need_labels) break;
+  if (fb != none) {
+    double p[3], q[3];
+    d2h(p, S.pos.get() + 3 * fb, 3, s);
+    d2h(q, S.nrm.get() + 3 * fb, 3, s);
+    PCR_CUDA(cudaStreamSynchronize(s));
+    if (!(std::isfinite(p[0]) && std::isfinite(p[1]) && std::isfinite(p[2])))
+      add("point_position_finite", fb, "non-finite position");
+    const double nn = norm(load3(q));
+    if (std::abs(nn - 1.0) > 1e-6) add("point_normal_unit", fb, "normal length " + std::to_string(nn));
   }
-  for (uint32_t i = 0; i < d.n_edges; ++i) {
-    const double* g = d.edge_geometry + 12ull * i;
-    const V3 s = load3(g), e = load3(g + 3), na = load3(g + 6), nb = load3(g + 9);
-    const double len = norm(e - s);
+  for (uint32_t i = 0; i < S.n_edges; ++i) {
+    const double* g = &S.h_edges[12ull * i];
+    const V3 st = load3(g), e = load3(g + 3), na = load3(g + 6), nb = load3(g + 9);
+    const double len = norm(e - st);
     if (!(len > 0.0)) {
       add("edge_nondegenerate", i, "zero-length edge");
       continue;
     }
-    const V3 w = (e - s) / len;
+    const V3 w = (e - st) / len;
     if (std::abs(norm(na) - 1.0) > 1e-6) add("edge_normal_a_unit", i, "normal_a not unit");
     if (std::abs(norm(nb) - 1.0) > 1e-6) add("edge_normal_b_unit", i, "normal_b not unit");
     if (std::abs(dot(w, na)) > 1e-3) add("edge_normal_a_perpendicular", i, "w.n_a = " + std::to_string(dot(w, na)));
     if (std::abs(dot(w, nb)) > 1e-3) add("edge_normal_b_perpendicular", i, "w.n_b = " + std::to_string(dot(w, nb)));
     if (norm(na - nb) < 1e-9) add("edge_wedge_defined", i, "adjacent normals coincide");
-    if (labels.count(d.edge_label[i]) > 0)
+    if (lh[i])
       add("edge_label_disjoint", i,
-          "edge label " + std::to_string(d.edge_label[i]) + " collides with a surface label");
+          "edge label " + std::to_string(S.h_edge_label[i]) + " collides with a surface label");
   }
-  auto radios = [&](const double* pos, const uint32_t* id, uint32_t n, const char* kind) {
+  auto radios = [&](const std::vector<double>& pos, const std::vector<uint32_t>& id, const char* kind) {
     std::unordered_set<uint32_t> ids;
-    for (uint32_t i = 0; i < n; ++i) {
-      if (!finite3(pos + 3ull * i)) add(std::string(kind) + "_position_finite", i, "non-finite position");
+    for (size_t i = 0; i < id.size(); ++i) {
+      const double* p = &pos[3 * i];
+      if (!(std::isfinite(p[0]) && std::isfinite(p[1]) && std::isfinite(p[2])))
+        add(std::string(kind) + "_position_finite", i, "non-finite position");
       if (!ids.insert(id[i]).second) add(std::string(kind) + "_id_unique", i, "duplicate id " + std::to_string(id[i]));
     }
   };
-  radios(d.tx_position, d.tx_id, d.n_tx, "tx");
-  radios(d.rx_position, d.rx_id, d.n_rx, "rx");
-  if (d.n_tx == 0) add("has_transmitter", 0, "no transmitters");
-  if (d.n_rx == 0) add("has_receiver", 0, "no receivers");
-  if (!(d.carrier_frequency_hz > 0.0)) add("carrier_frequency_positive", 0, "frequency must be > 0");
+  radios(S.h_tx, S.h_tx_id, "tx");
+  radios(S.h_rx, S.h_rx_id, "rx");
+  if (S.h_tx_id.empty()) add("has_transmitter", 0, "no transmitters");
+  if (S.h_rx_id.empty()) add("has_receiver", 0, "no receivers");
+  if (!(S.carrier_frequency_hz > 0.0)) add("carrier_frequency_positive", 0, "frequency must be > 0");
   if (out.empty()) return false;
   v = out.front();
   return true;
@@ -284,7 +320,51 @@ void run_config_defaults(pcr_run_config* c) {
   c->fresnel_enabled = 1;
 }
 
+void run_pipeline_core(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, pcr_summary** out,
+                       double upload_seconds);
+
+void upload_scene(Ctx& ctx, const pcr_scene_desc& d, SceneDev& S) {
+  cudaStream_t s = ctx.stream;
+  const size_t n = d.n_points;
+  S.n_points = n;
+  S.pos.alloc(3 * n + 3, s);
+  S.nrm.alloc(3 * n + 3, s);
+  S.label.alloc(n + 1, s);
+  h2d(S.pos.get(), d.point_position, 3 * n, s);
+  h2d(S.nrm.get(), d.point_normal, 3 * n, s);
+  h2d(S.label.get(), d.point_label, n, s);
+  S.n_edges = d.n_edges;
+  S.h_edges.assign(d.edge_geometry, d.edge_geometry + 12ull * d.n_edges);
+  S.h_edge_label.assign(d.edge_label, d.edge_label + d.n_edges);
+  S.edges.alloc(12ull * d.n_edges + 12, s);
+  S.edge_label.alloc(d.n_edges + 1ull, s);
+  h2d(S.edges.get(), S.h_edges.data(), S.h_edges.size(), s);
+  h2d(S.edge_label.get(), S.h_edge_label.data(), S.h_edge_label.size(), s);
+  S.h_tx.assign(d.tx_position, d.tx_position + 3ull * d.n_tx);
+  S.h_tx_id.assign(d.tx_id, d.tx_id + d.n_tx);
+  S.h_rx.assign(d.rx_position, d.rx_position + 3ull * d.n_rx);
+  S.h_rx_id.assign(d.rx_id, d.rx_id + d.n_rx);
+  S.rx_pos.alloc(3ull * d.n_rx + 3, s);
+  S.rx_id.alloc(d.n_rx + 1ull, s);
+  h2d(S.rx_pos.get(), S.h_rx.data(), S.h_rx.size(), s);
+  h2d(S.rx_id.get(), S.h_rx_id.data(), S.h_rx_id.size(), s);
+  S.carrier_frequency_hz = d.carrier_frequency_hz;
+  PCR_CUDA(cudaStreamSynchronize(s));
+}
+
 void api_run_pipeline_on_scene(Ctx& ctx, const pcr_scene_desc& desc, const pcr_run_config& cfg, pcr_summary** out) {
+  auto t0 = Clock::now();
+  SceneDev scene;
+  upload_scene(ctx, desc, scene);
+  run_pipeline_core(ctx, scene, cfg, out, since(t0));
+}
+
+void api_run_pipeline_device(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, pcr_summary** out) {
+  run_pipeline_core(ctx, scene, cfg, out, 0.0);
+}
+
+void run_pipeline_core(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, pcr_summary** out,
+                       double upload_seconds) {
   cudaStream_t s = ctx.stream;
   pcr_summary* S = halloc<pcr_summary>(1);
   auto fail = [&](const char* stage, const std::exception& e) {
@@ -302,46 +382,30 @@ void api_run_pipeline_on_scene(Ctx& ctx, const pcr_scene_desc& desc, const pcr_r
     }
   };
   S->hash = config_hash(cfg);
-  S->point_count = desc.n_points;
-  S->edge_count = desc.n_edges;
+  S->point_count = scene.n_points;
+  S->edge_count = scene.n_edges;
+  const uint32_t n_tx = static_cast<uint32_t>(scene.h_tx_id.size());
 
   auto t0 = Clock::now();
-  Violation v;
-  if (first_violation(desc, v)) {
-    std::free(S);
-    throw Error(PCR_ERR_RUNTIME, "validate: " + v.rule + " (" + v.detail + ")");
+  {
+    Violation v;
+    bool bad = false;
+    try {
+      bad = first_violation_device(ctx, scene, v);
+    } catch (const std::exception& e) {
+      fail("validate", e);
+    }
+    if (bad) {
+      std::free(S);
+      throw Error(PCR_ERR_RUNTIME, "validate: " + v.rule + " (" + v.detail + ")");
+    }
   }
-  timing("validate", since(t0));
+  timing("validate", since(t0) + upload_seconds);
 
-  // upload + voxelize
   t0 = Clock::now();
-  SceneDev scene;
   GridDev grid;
   try {
-    const size_t n = desc.n_points;
-    scene.n_points = n;
-    scene.pos.alloc(3 * n + 3, s);
-    scene.nrm.alloc(3 * n + 3, s);
-    scene.label.alloc(n + 1, s);
-    h2d(scene.pos.get(), desc.point_position, 3 * n, s);
-    h2d(scene.nrm.get(), desc.point_normal, 3 * n, s);
-    h2d(scene.label.get(), desc.point_label, n, s);
-    scene.n_edges = desc.n_edges;
-    scene.h_edges.assign(desc.edge_geometry, desc.edge_geometry + 12ull * desc.n_edges);
-    scene.h_edge_label.assign(desc.edge_label, desc.edge_label + desc.n_edges);
-    scene.edges.alloc(12ull * desc.n_edges + 12, s);
-    scene.edge_label.alloc(desc.n_edges + 1ull, s);
-    h2d(scene.edges.get(), scene.h_edges.data(), scene.h_edges.size(), s);
-    h2d(scene.edge_label.get(), scene.h_edge_label.data(), scene.h_edge_label.size(), s);
-    scene.h_tx.assign(desc.tx_position, desc.tx_position + 3ull * desc.n_tx);
-    scene.h_tx_id.assign(desc.tx_id, desc.tx_id + desc.n_tx);
-    scene.h_rx.assign(desc.rx_position, desc.rx_position + 3ull * desc.n_rx);
-    scene.h_rx_id.assign(desc.rx_id, desc.rx_id + desc.n_rx);
-    scene.rx_pos.alloc(3ull * desc.n_rx + 3, s);
-    scene.rx_id.alloc(desc.n_rx + 1ull, s);
-    h2d(scene.rx_pos.get(), scene.h_rx.data(), scene.h_rx.size(), s);
-    h2d(scene.rx_id.get(), scene.h_rx_id.data(), scene.h_rx_id.size(), s);
-    scene.carrier_frequency_hz = desc.carrier_frequency_hz;
+    KTimer kt(ctx, "build_grid");
     build_grid_device(ctx, scene, cfg.voxel_size_m, cfg.division_factor, uint64_t(1) << 27, grid);
   } catch (const std::exception& e) {
     fail("voxelize", e);
@@ -362,11 +426,11 @@ void api_run_pipeline_on_scene(Ctx& ctx, const pcr_scene_desc& desc, const pcr_r
   CandSet cs;
   cs.stride = stride;
   try {
-    std::vector<TxDev> txs(desc.n_tx);
-    std::vector<CandDev> props(desc.n_tx);
+    std::vector<TxDev> txs(n_tx);
+    std::vector<CandDev> props(n_tx);
     TraceStats st;
     uint64_t total = 0;
-    for (uint32_t t = 0; t < desc.n_tx; ++t) {
+    for (uint32_t t = 0; t < n_tx; ++t) {
       transmission_device(ctx, grid, scene, t, txs[t]);
       propagate_device(ctx, grid, scene, t, txs[t].hit_ie.get(), txs[t].hit_kind.get(), txs[t].hit_pos.get(),
                        txs[t].hit_nrm.get(), txs[t].hit_inc.get(), txs[t].n_hits, tp, props[t], st);
@@ -380,6 +444,8 @@ void api_run_pipeline_on_scene(Ctx& ctx, const pcr_scene_desc& desc, const pcr_r
       S->visibility_tests += grid.n_ies;
     }
     S->cone_traces = st.cone_traces;
+    S->walk_cells = st.walk_cells;
+    S->walk_ies = st.walk_ies;
     S->visibility_tests += st.visibility_tests;
     if (total > 0xffffffffull) throw Error(PCR_ERR_NOMEM, "too many candidates");
     cs.n = static_cast<uint32_t>(total);
@@ -404,11 +470,11 @@ void api_run_pipeline_on_scene(Ctx& ctx, const pcr_scene_desc& desc, const pcr_r
     PCR_CUDA(cudaMemsetAsync(cs.nrm.get(), 0, 3 * ms * sizeof(double), s));
     uint32_t row = 0;
     const GridView gv = grid.view();
-    for (uint32_t t = 0; t < desc.n_tx; ++t) {
-      const V3 txp = load3(desc.tx_position + 3ull * t);
+    for (uint32_t t = 0; t < n_tx; ++t) {
+      const V3 txp = load3(&scene.h_tx[3ull * t]);
       if (txs[t].n_los) {
         count_launch();
-        los_rows_kernel<<<nb(txs[t].n_los), 256, 0, s>>>(txs[t].los_ie.get(), txs[t].n_los, gv, txp, desc.tx_id[t], row,
+        los_rows_kernel<<<nb(txs[t].n_los), 256, 0, s>>>(txs[t].los_ie.get(), txs[t].n_los, gv, txp, scene.h_tx_id[t], row,
                                                           cs.rx_id.get(), cs.rx_pos.get(), cs.length.get(),
                                                           cs.n_inter.get(), cs.tx_id.get(), cs.tx_pos.get());
         PCR_LAUNCH_CHECK();
@@ -428,7 +494,7 @@ void api_run_pipeline_on_scene(Ctx& ctx, const pcr_scene_desc& desc, const pcr_r
         PCR_CUDA(cudaMemcpyAsync(cs.pos.get() + 3 * q, c.pos.get(), 3 * cnt * sizeof(double), cudaMemcpyDeviceToDevice, s));
         PCR_CUDA(cudaMemcpyAsync(cs.nrm.get() + 3 * q, c.nrm.get(), 3 * cnt * sizeof(double), cudaMemcpyDeviceToDevice, s));
         count_launch();
-        tx_rows_kernel<<<nb(c.n), 256, 0, s>>>(c.n, row, txp, desc.tx_id[t], cs.tx_id.get(), cs.tx_pos.get());
+        tx_rows_kernel<<<nb(c.n), 256, 0, s>>>(c.n, row, txp, scene.h_tx_id[t], cs.tx_id.get(), cs.tx_pos.get());
         PCR_LAUNCH_CHECK();
         row += c.n;
       }
@@ -449,6 +515,8 @@ void api_run_pipeline_on_scene(Ctx& ctx, const pcr_scene_desc& desc, const pcr_r
                    cs.length.get(), cs.n_inter.get(), cs.label.get(), cs.edge.get(), cs.kind.get()};
     RefineDevOut ro;
     refine_device(ctx, grid, scene, in, rp, ro);
+    S->refine_trials = ro.trials;
+    S->refine_marches = ro.marches;
     const size_t n = cs.n, ms = n * stride;
     std::vector<uint8_t> has(n), kind(ms);
     std::vector<int32_t> reason(n);

@@ -20,6 +20,8 @@ void api_refine_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, cons
                       const pcr_refine_params& p, pcr_outcomes** out);
 // pipeline (pipeline.cu)
 void api_run_pipeline_on_scene(Ctx& ctx, const pcr_scene_desc& desc, const pcr_run_config& cfg, pcr_summary** out);
+void api_run_pipeline_device(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, pcr_summary** out);
+void upload_scene(Ctx& ctx, const pcr_scene_desc& d, SceneDev& S);
 uint64_t config_hash(const pcr_run_config& c);
 void run_config_defaults(pcr_run_config* c);
 

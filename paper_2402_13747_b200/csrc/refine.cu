@@ -70,7 +70,7 @@ __device__ __forceinline__ int voxel_floor(double p, double o, double vs) {
 
 // reproject (refine.cpp:80-130) with surface_ies_near (:34-52) scanned in place.
 __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, const GridView& g, const SceneView& s,
-                          Reproj& out) {
+                          Reproj& out, uint32_t& n_march) {
   const V3 diff = predicted - prev;
   const double dist = norm(diff);
   if (dist < kTiny) return false;
@@ -100,6 +100,7 @@ __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, c
             if (!(norm(ld3(sc4) - predicted) <= radius + sc4.w)) continue;
             if (same != (g.ie_label[i] == label)) continue;
             SurfaceHit hit;
+            ++n_march;
             if (!march_segment(prev, dir, i, g, s, inf, &hit)) continue;
             if (hit.distance >= best_t) continue;
             best_t = hit.distance;
@@ -133,6 +134,7 @@ __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, c
             const double d = norm(sc - predicted);
             if (d >= best_d) continue;
             SurfaceHit hit;
+            ++n_march;
             if (!project_to_surface(predicted, i, g, s, &hit)) continue;
             best_d = d;
             best = Reproj{hit.position, hit.normal, g.ie_label[i]};
@@ -172,7 +174,51 @@ struct RefOut {
   double* delay;
   double* gnorm;
   uint32_t* iters;
+  unsigned long long* stats;  // [0] trials, [1] reprojection marches
 };
+
+// Dynamic state of a path between iterations: reflection nodes are (c, normal,
+// label) with r = s = 0 and (u, v) = local_frame(normal); diffraction nodes are t.
+// The iteration is a pure function of it, so a bitwise repeat means the trajectory
+// is periodic and can never reach ||g|| < delta (every state of the cycle already
+// failed the test) — the reference would spin to rho and report not_converged.
+struct Snapshot {
+  double v[kMaxDepth][7];
+};
+
+__device__ __forceinline__ void take_snapshot(Snapshot& sn, const RNode* nd, int d) {
+  for (int q = 0; q < d; ++q) {
+    if (nd[q].kind == 0) {
+      sn.v[q][0] = nd[q].c.x;
+      sn.v[q][1] = nd[q].c.y;
+      sn.v[q][2] = nd[q].c.z;
+      sn.v[q][3] = nd[q].n.x;
+      sn.v[q][4] = nd[q].n.y;
+      sn.v[q][5] = nd[q].n.z;
+      sn.v[q][6] = __longlong_as_double(static_cast<long long>(nd[q].label));
+    } else {
+      sn.v[q][0] = nd[q].p0;
+    }
+  }
+}
+
+__device__ __forceinline__ bool same_snapshot(const Snapshot& sn, const RNode* nd, int d) {
+  for (int q = 0; q < d; ++q) {
+    if (nd[q].kind == 0) {
+      if (__double_as_longlong(sn.v[q][0]) != __double_as_longlong(nd[q].c.x) ||
+          __double_as_longlong(sn.v[q][1]) != __double_as_longlong(nd[q].c.y) ||
+          __double_as_longlong(sn.v[q][2]) != __double_as_longlong(nd[q].c.z) ||
+          __double_as_longlong(sn.v[q][3]) != __double_as_longlong(nd[q].n.x) ||
+          __double_as_longlong(sn.v[q][4]) != __double_as_longlong(nd[q].n.y) ||
+          __double_as_longlong(sn.v[q][5]) != __double_as_longlong(nd[q].n.z) ||
+          static_cast<uint32_t>(__double_as_longlong(sn.v[q][6])) != nd[q].label)
+        return false;
+    } else if (__double_as_longlong(sn.v[q][0]) != __double_as_longlong(nd[q].p0)) {
+      return false;
+    }
+  }
+  return true;
+}
 
 __global__ void __launch_bounds__(128) refine_kernel(CandIn in, uint32_t n, GridView g, SceneView s, double delta,
                                                      int rho, double step_size, RefOut o) {
@@ -222,6 +268,16 @@ __global__ void __launch_bounds__(128) refine_kernel(CandIn in, uint32_t n, Grid
   double gnorm = 0.0;
   bool converged = false;
   int iter = 0;
+  uint32_t n_trials = 0, n_march = 0;
+  auto flush = [&]() {
+    atomicAdd(o.stats, static_cast<unsigned long long>(n_trials));
+    atomicAdd(o.stats + 1, static_cast<unsigned long long>(n_march));
+  };
+  // Brent cycle detection on the post-iteration state
+  Snapshot saved;
+  take_snapshot(saved, nd, d);
+  int power = 1, lam = 0;
+  bool stalled = false;
   for (; iter < rho; ++iter) {
     // local_gradients
     double gr[2 * kMaxDepth];
@@ -235,6 +291,7 @@ __global__ void __launch_bounds__(128) refine_kernel(CandIn in, uint32_t n, Grid
       if (lp < kTiny || ln < kTiny) {
         o.reason[k] = PCR_DEGENERATE;
         o.iters[k] = iter + 1;
+        flush();
         return;
       }
       const V3 e_sum = dp / lp + dn / ln;
@@ -269,6 +326,7 @@ __global__ void __launch_bounds__(128) refine_kernel(CandIn in, uint32_t n, Grid
         }
         tpts[q] = node_point(nd[q], tp0[q], tp1[q]);
       }
+      ++n_trials;
       if (chain_len(tx, tpts, d, rx) <= f + 1e-15) {
         accepted = true;
         break;
@@ -276,7 +334,7 @@ __global__ void __launch_bounds__(128) refine_kernel(CandIn in, uint32_t n, Grid
       step *= 0.5;
     }
     if (!accepted) {
-      iter = rho;  // fixed point: every remaining iteration repeats this one
+      stalled = true;  // fixed point: every remaining iteration repeats this one
       break;
     }
     for (int q = 0; q < d; ++q) {
@@ -289,9 +347,10 @@ __global__ void __launch_bounds__(128) refine_kernel(CandIn in, uint32_t n, Grid
       const V3 prev = q == 0 ? tx : node_point(nd[q - 1], nd[q - 1].p0, nd[q - 1].p1);
       const V3 predicted = node_point(nd[q], nd[q].p0, nd[q].p1);
       Reproj re;
-      if (!reproject(prev, predicted, nd[q].label, g, s, re)) {
+      if (!reproject(prev, predicted, nd[q].label, g, s, re, n_march)) {
         o.reason[k] = PCR_RAY_MISSED;
         o.iters[k] = iter + 1;
+        flush();
         return;
       }
       nd[q].c = re.pos;
@@ -303,8 +362,18 @@ __global__ void __launch_bounds__(128) refine_kernel(CandIn in, uint32_t n, Grid
     }
     for (int q = 0; q < d; ++q) pts[q] = node_point(nd[q], nd[q].p0, nd[q].p1);
     f = chain_len(tx, pts, d, rx);
+    if (same_snapshot(saved, nd, d)) {
+      stalled = true;  // periodic trajectory: never converges (see Snapshot)
+      break;
+    }
+    if (++lam == power) {
+      take_snapshot(saved, nd, d);
+      power <<= 1;
+      lam = 0;
+    }
   }
-  o.iters[k] = static_cast<uint32_t>(converged ? iter + 1 : iter);
+  o.iters[k] = static_cast<uint32_t>(converged || stalled ? iter + 1 : iter);  // iterations executed
+  flush();
   if (!converged) {
     o.reason[k] = PCR_NOT_CONVERGED;
     return;
@@ -359,11 +428,22 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
   PCR_CUDA(cudaMemcpyAsync(out.label.get(), in.label, ms * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
   if (!in.n) return;
   CandIn ci{in.stride, in.tx, in.rx, in.n_inter, in.kind, in.pos, in.label, in.nrm, in.edge, in.coarse_length};
+  DBuf<unsigned long long> stats(2, s);
+  PCR_CUDA(cudaMemsetAsync(stats.get(), 0, 2 * sizeof(unsigned long long), s));
   RefOut ro{out.reason.get(), out.has_path.get(), out.pos.get(), out.nrm.get(), out.label.get(),
-            out.length.get(), out.delay.get(), out.gnorm.get(), out.iters.get()};
+            out.length.get(), out.delay.get(), out.gnorm.get(), out.iters.get(), stats.get()};
   count_launch();
-  refine_kernel<<<nb(in.n, 128), 128, 0, s>>>(ci, in.n, grid.view(), scene.view(), p.delta, p.rho, p.step_size, ro);
+  {
+    KTimer kt(ctx, "refine");
+    refine_kernel<<<nb(in.n, 128), 128, 0, s>>>(ci, in.n, grid.view(), scene.view(), p.delta, p.rho, p.step_size,
+                                                ro);
+  }
   PCR_LAUNCH_CHECK();
+  unsigned long long hs[2];
+  d2h(hs, stats.get(), 2, s);
+  PCR_CUDA(cudaStreamSynchronize(s));
+  out.trials = hs[0];
+  out.marches = hs[1];
 }
 
 void api_refine_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const pcr_paths& c,

@@ -13,7 +13,7 @@
 
 namespace pcr {
 
-uint64_t g_launch_count = 0;
+uint64_t g_launch_count = 0, g_h2d_bytes = 0, g_d2h_bytes = 0;
 
 namespace {
 

@@ -18,7 +18,7 @@ struct TxDev {
 
 // Work counters of a propagate call (SURVEY §8d units).
 struct TraceStats {
-  uint64_t cone_traces = 0, visibility_tests = 0;
+  uint64_t cone_traces = 0, visibility_tests = 0, walk_cells = 0, walk_ies = 0;
 };
 
 // Kept propagation candidates of one TX in output (DFS) order; interaction
@@ -43,6 +43,7 @@ struct RefineDevOut {
   DBuf<uint8_t> has_path;
   DBuf<double> pos, nrm, length, delay, gnorm;
   DBuf<uint32_t> label, iters;
+  uint64_t trials = 0, marches = 0;  // work counters (summed over candidates)
 };
 
 void transmission_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint32_t tx_index, TxDev& out);

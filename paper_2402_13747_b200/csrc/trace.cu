@@ -127,24 +127,33 @@ __global__ void materialize_kernel(const Node* __restrict__ nodes, uint32_t node
 // edges once the diffraction budget is spent): the reference traces them and
 // discards the reception (tracer.cpp:441, 456), so the output is unchanged.
 __global__ void walk_kernel(const Ray* __restrict__ rays, uint32_t n_rays, GridView g, TraceCfg c, bool filter,
-                            Task* __restrict__ tasks, uint32_t* __restrict__ n_tasks, uint32_t cap) {
+                            Task* __restrict__ tasks, uint32_t* __restrict__ n_tasks, uint32_t cap,
+                            unsigned long long* __restrict__ stats) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n_rays) return;
-  const Ray r = rays[k];
-  if (!r.alive) return;
-  const bool can_refl = r.depth < c.max_interactions;
-  const bool can_diff = can_refl && r.dc < c.max_diffractions;
-  cone_walk(
-      g, r, [](uint32_t) {},
-      [&](uint32_t i) {
-        if (filter) {
-          const uint32_t kind = g.ie_meta[i] & 3u;
-          if (kind == kSurface && !can_refl) return;
-          if (kind == kEdge && !can_diff) return;
-        }
-        const uint32_t slot = atomic_append(n_tasks);
-        if (slot < cap) tasks[slot] = Task{k, i};
-      });
+  uint32_t cells = 0, ies = 0;
+  if (k < n_rays) {
+    const Ray r = rays[k];
+    if (r.alive) {
+      const bool can_refl = r.depth < c.max_interactions;
+      const bool can_diff = can_refl && r.dc < c.max_diffractions;
+      cone_walk(
+          g, r, [](uint32_t) {},
+          [&](uint32_t i) {
+            if (filter) {
+              const uint32_t kind = g.ie_meta[i] & 3u;
+              if (kind == kSurface && !can_refl) return;
+              if (kind == kEdge && !can_diff) return;
+            }
+            const uint32_t slot = atomic_append(n_tasks);
+            if (slot < cap) tasks[slot] = Task{k, i};
+          },
+          &cells, &ies);
+    }
+  }
+  if (stats) {
+    warp_add_u64(stats, cells);
+    warp_add_u64(stats + 1, ies);
+  }
 }
 
 struct SpawnOut {
@@ -646,8 +655,11 @@ void transmission_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, u
   DBuf<double> hp(3 * m, s), hn(3 * m, s), hi(3 * m, s);
   if (n) {
     count_launch();
-    transmission_kernel<<<nb(n, 128), 128, 0, s>>>(grid.view(), scene.view(), tx,
-                                                   TxOut{los.get(), hit.get(), hp.get(), hn.get(), hi.get()});
+    {
+      KTimer kt(ctx, "transmission");
+      transmission_kernel<<<nb(n, 128), 128, 0, s>>>(grid.view(), scene.view(), tx,
+                                                     TxOut{los.get(), hit.get(), hp.get(), hn.get(), hi.get()});
+    }
     PCR_LAUNCH_CHECK();
   }
   DBuf<uint32_t> f(m, s), lpos(m, s), hpos(m, s), tot(2, s);
@@ -808,6 +820,8 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
   size_t task_cap = 8ull * chunk;
   DBuf<Task> tasks(task_cap, s);
   DBuf<unsigned long long> alive(1, s);
+  DBuf<unsigned long long> walk_stats(2, s);
+  PCR_CUDA(cudaMemsetAsync(walk_stats.get(), 0, 2 * sizeof(unsigned long long), s));
 
   std::vector<StackEntry> stack;
   auto push_range = [&](uint32_t begin, uint32_t count) {
@@ -837,8 +851,11 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
     }
     const uint32_t nr = static_cast<uint32_t>(std::min<uint64_t>(chunk, top.v_total - top.v_done));
     count_launch();
-    materialize_kernel<<<nb(nr), kT, 0, s>>>(nodes.get(), top.node_begin, top.prefix.get(), top.n_nodes, top.v_done,
-                                             nr, gv, sv, c, fan, rays.get());
+    {
+      KTimer kt(ctx, "materialize");
+      materialize_kernel<<<nb(nr), kT, 0, s>>>(nodes.get(), top.node_begin, top.prefix.get(), top.n_nodes,
+                                               top.v_done, nr, gv, sv, c, fan, rays.get());
+    }
     PCR_LAUNCH_CHECK();
     top.v_done += nr;
     PCR_CUDA(cudaMemsetAsync(alive.get(), 0, sizeof(unsigned long long), s));
@@ -849,8 +866,11 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
     for (;;) {
       PCR_CUDA(cudaMemsetAsync(counters.get(), 0, sizeof(uint32_t), s));
       count_launch();
-      walk_kernel<<<nb(nr, 128), 128, 0, s>>>(rays.get(), nr, gv, c, true, tasks.get(), counters.get(),
-                                              static_cast<uint32_t>(task_cap));
+      {
+        KTimer kt(ctx, "cone_walk");
+        walk_kernel<<<nb(nr, 128), 128, 0, s>>>(rays.get(), nr, gv, c, true, tasks.get(), counters.get(),
+                                                static_cast<uint32_t>(task_cap), walk_stats.get());
+      }
       PCR_LAUNCH_CHECK();
       d2h(&n_tasks, counters.get(), 1, s);
       PCR_CUDA(cudaStreamSynchronize(s));
@@ -881,9 +901,12 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
     uint32_t h_cnt[2] = {n_nodes, n_cands};
     h2d(counters.get(), h_cnt, 2, s);
     count_launch();
-    visibility_kernel<<<nb(n_tasks, 128), 128, 0, s>>>(
-        tasks.get(), n_tasks, rays.get(), nodes.get(), gv, sv, c,
-        SpawnOut{nodes.get(), counters.get(), cands.get(), counters.get() + 1, nullptr});
+    {
+      KTimer kt(ctx, "visibility");
+      visibility_kernel<<<nb(n_tasks, 128), 128, 0, s>>>(
+          tasks.get(), n_tasks, rays.get(), nodes.get(), gv, sv, c,
+          SpawnOut{nodes.get(), counters.get(), cands.get(), counters.get() + 1, nullptr});
+    }
     PCR_LAUNCH_CHECK();
     d2h(h_cnt, counters.get(), 2, s);
     PCR_CUDA(cudaStreamSynchronize(s));
@@ -906,7 +929,10 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
 
   DBuf<Cand> kept;
   uint32_t nk = 0;
-  kappa_select(ctx, grid, cands, n_cands, nodes.get(), L, c.kappa, kept, nk);
+  {
+    KTimer kt(ctx, "kappa_select");
+    kappa_select(ctx, grid, cands, n_cands, nodes.get(), L, c.kappa, kept, nk);
+  }
   out.n = nk;
   const size_t m = nk ? nk : 1;
   const size_t ms = m * out.stride;
@@ -935,7 +961,11 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
                                                    co);
     PCR_LAUNCH_CHECK();
   }
+  unsigned long long ws[2] = {0, 0};
+  d2h(ws, walk_stats.get(), 2, s);
   PCR_CUDA(cudaStreamSynchronize(s));
+  stats.walk_cells += ws[0];
+  stats.walk_ies += ws[1];
 }
 
 // ---- C-ABI adapters ---------------------------------------------------------------------
@@ -1068,7 +1098,7 @@ void api_cone_trace_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, 
     if (n_rays) {
       count_launch();
       walk_kernel<<<nb(n_rays, 128), 128, 0, s>>>(rays.get(), static_cast<uint32_t>(n_rays), gv, c, false,
-                                                  tasks.get(), cnt.get(), static_cast<uint32_t>(cap));
+                                                  tasks.get(), cnt.get(), static_cast<uint32_t>(cap), nullptr);
       PCR_LAUNCH_CHECK();
     }
     d2h(&nt, cnt.get(), 1, s);

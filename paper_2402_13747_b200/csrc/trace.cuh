@@ -59,8 +59,10 @@ __device__ __forceinline__ bool passes_planes(const Ray& r, const V3& q) {
 // it lies in N(u) for an earlier evaluating voxel u within Chebyshev distance 2
 // of v, and those u are a suffix of at most 6 voxels.
 template <typename OnEval, typename OnIE>
-__device__ __forceinline__ void cone_walk(const GridView& g, const Ray& r, OnEval on_eval, OnIE on_ie) {
+__device__ __forceinline__ void cone_walk(const GridView& g, const Ray& r, OnEval on_eval, OnIE on_ie,
+                                          uint32_t* n_cells = nullptr, uint32_t* n_ies = nullptr) {
   if (g.n_ies == 0) return;
+  uint32_t cells_seen = 0, ies_seen = 0;
   const double half_angle = 0.5 * r.apex;
   const double exempt_radius = 2.0 * g.sub_radius;
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
@@ -87,9 +89,11 @@ __device__ __forceinline__ void cone_walk(const GridView& g, const Ray& r, OnEva
             if (seen) continue;
             const uint32_t ni = linear_index(g, nx, ny, nz);
             on_eval(ni);
+            ++cells_seen;
             const int4 cell = g.cells[ni];
             if (cell.x == cell.y) continue;
             if (!cone_intersects_sphere(r.o, r.d, half_angle, voxel_center(g, nx, ny, nz), g.voxel_radius)) continue;
+            ies_seen += static_cast<uint32_t>(cell.y - cell.x);
             for (uint32_t i = static_cast<uint32_t>(cell.x); i < static_cast<uint32_t>(cell.y); ++i) {
               if (i == r.origin_ie) continue;
               const double4 sc4 = g.ie_sc[i];
@@ -134,6 +138,15 @@ __device__ __forceinline__ void cone_walk(const GridView& g, const Ray& r, OnEva
       w.advance(g);
     }
   }
+  if (n_cells) *n_cells += cells_seen;
+  if (n_ies) *n_ies += ies_seen;
+}
+
+// Warp-aggregated 64-bit counter add.
+__device__ __forceinline__ void warp_add_u64(unsigned long long* dst, unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
 }
 
 }  // namespace pcr

@@ -62,6 +62,13 @@ def lib():
                                                 C.c_uint64, pp(C.c_uint8)]
         L.pcr_refine_batch.argtypes = [vp, vp, vp, pp(abi.Paths), pp(abi.RefineParams), pp(pp(abi.Outcomes))]
         L.pcr_run_pipeline_on_scene.argtypes = [vp, pp(abi.SceneDesc), pp(abi.RunConfig), pp(pp(abi.Summary))]
+        L.pcr_run_pipeline_device.argtypes = [vp, vp, pp(abi.RunConfig), pp(pp(abi.Summary))]
+        L.pcr_stream.restype = vp
+        L.pcr_stream.argtypes = [vp]
+        L.pcr_set_profiling.argtypes = [vp, C.c_int]
+        L.pcr_kernel_times.argtypes = [vp, vp, pp(C.c_double), pp(C.c_uint64), C.c_int, C.c_int]
+        L.pcr_transfer_bytes.argtypes = [pp(C.c_uint64), pp(C.c_uint64)]
+        L.pcr_fp64_probe.argtypes = [vp, pp(C.c_double)]
         L.pcr_config_hash.restype = C.c_uint64
         L.pcr_config_hash.argtypes = [pp(abi.RunConfig)]
         L.pcr_run_config_defaults.argtypes = [pp(abi.RunConfig)]
@@ -276,6 +283,56 @@ def run_pipeline_on_scene(scene: Scene, config: RunConfig | None = None, ctx: Co
         return abi.summary_to_dict(out.contents)
     finally:
         lib().pcr_free_summary(out)
+
+
+def run_pipeline_device(scene: DeviceScene, config: RunConfig | None = None) -> dict:
+    """run_pipeline_on_scene over a scene already resident in HBM (pcr_run_pipeline_device)."""
+    config = config or default_run_config()
+    out = C.POINTER(abi.Summary)()
+    scene.ctx.check(lib().pcr_run_pipeline_device(scene.ctx.handle, scene.handle, C.byref(config), C.byref(out)))
+    try:
+        return abi.summary_to_dict(out.contents)
+    finally:
+        lib().pcr_free_summary(out)
+
+
+def stream_ptr(ctx: Context | None = None) -> int:
+    """cudaStream_t the library launches on (for caller-side CUDA events)."""
+    ctx = ctx or Context.default()
+    return int(lib().pcr_stream(ctx.handle) or 0)
+
+
+def set_profiling(on: bool, ctx: Context | None = None) -> None:
+    ctx = ctx or Context.default()
+    ctx.check(lib().pcr_set_profiling(ctx.handle, int(on)))
+
+
+def kernel_times(reset: bool = True, ctx: Context | None = None) -> dict:
+    """Per-kernel CUDA-event totals since the last reset: {name: (ms, launches)}."""
+    ctx = ctx or Context.default()
+    cap = 64
+    names = (C.c_char * 32 * cap)()
+    ms = (C.c_double * cap)()
+    launches = (C.c_uint64 * cap)()
+    n = lib().pcr_kernel_times(ctx.handle, names, ms, launches, cap, int(reset))
+    if n < 0:
+        ctx.check(-n)
+    return {names[i].value.decode(): (float(ms[i]), int(launches[i])) for i in range(n)}
+
+
+def transfer_bytes() -> tuple[int, int]:
+    """(host->device, device->host) bytes the library copied so far in this process."""
+    a, b = C.c_uint64(), C.c_uint64()
+    lib().pcr_transfer_bytes(C.byref(a), C.byref(b))
+    return int(a.value), int(b.value)
+
+
+def fp64_probe(ctx: Context | None = None) -> float:
+    """Measured non-FMA FP64 throughput of the device, TFLOP/s."""
+    ctx = ctx or Context.default()
+    v = C.c_double()
+    ctx.check(lib().pcr_fp64_probe(ctx.handle, C.byref(v)))
+    return float(v.value)
 
 
 def config_hash(config: RunConfig) -> int:
