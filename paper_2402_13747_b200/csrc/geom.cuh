@@ -379,4 +379,92 @@ __device__ inline bool segment_visible(const V3& origin, const V3& target, uint3
   return true;
 }
 
+// Warp-cooperative segment_visible (same arguments in every lane, same result): at
+// each walker step the lanes take the new cells (27 at the first voxel, the 9-cell
+// far slab afterwards), apply the cell prefilter, and the surviving cells' IEs are
+// flattened across lanes in rounds of 32; any blocker ends the walk for the warp.
+__device__ inline bool warp_segment_visible(const V3& origin, const V3& target, uint32_t target_ie,
+                                            const GridView& g, const SceneView& s) {
+  const int lane = threadIdx.x & 31;
+  const V3 diff = target - origin;
+  const double dist = norm(diff);
+  if (dist < kTiny) return true;
+  const V3 d = diff / dist;
+  const double er = g.sub_radius;
+  const double span = dist - 2.0 * er;
+  if (span <= 1e-9) return true;
+  const V3 o2 = origin + er * d;
+  const double cell_reach = g.voxel_radius + g.sub_radius;
+  Walker w;
+  w.init(g, origin, d, 0.0, dist);
+  int axis = -1;
+  while (w.active) {
+    int off[3];
+    bool mine;
+    if (axis < 0) {
+      mine = lane < 27;
+      off[0] = lane % 3 - 1;
+      off[1] = (lane / 3) % 3 - 1;
+      off[2] = lane / 9 - 1;
+    } else {
+      mine = lane < 9;
+      const int u = lane % 3 - 1, v = (lane / 3) % 3 - 1;
+      off[axis] = w.step[axis];
+      off[(axis + 1) % 3] = u;
+      off[(axis + 2) % 3] = v;
+    }
+    const int nx = w.v[0] + off[0], ny = w.v[1] + off[1], nz = w.v[2] + off[2];
+    int b = 0, cnt = 0;
+    if (mine && in_bounds(g, nx, ny, nz)) {
+      const int4 cell = g.cells[linear_index(g, nx, ny, nz)];
+      if (cell.x != cell.y) {
+        const V3 cc = voxel_center(g, nx, ny, nz);
+        const double tcc = sclamp(dot(cc - o2, d), 0.0, span);
+        if (!(norm((o2 + tcc * d) - cc) > cell_reach)) {
+          b = cell.x;
+          cnt = cell.y - cell.x;
+        }
+      }
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int base = 0; base < total; base += 32) {
+      const int f = base + lane;
+      int jlo = 0, jhi = 31;
+#pragma unroll
+      for (int st = 0; st < 5; ++st) {
+        const int mid = (jlo + jhi) >> 1;
+        const int vv = __shfl_sync(0xffffffffu, incl, mid);
+        if (vv > f) jhi = mid;
+        else jlo = mid + 1;
+      }
+      const int cb = __shfl_sync(0xffffffffu, b, jlo);
+      const int ce = __shfl_sync(0xffffffffu, incl - cnt, jlo);
+      bool blocked = false;
+      if (f < total) {
+        const uint32_t i = static_cast<uint32_t>(cb + (f - ce));
+        if ((g.ie_meta[i] & 3u) == kSurface && i != target_ie) {
+          const double4 sc4 = g.ie_sc[i];
+          const V3 sc = ld3(sc4);
+          const double tc = sclamp(dot(sc - o2, d), 0.0, span);
+          if (!(norm((o2 + tc * d) - sc) > sc4.w)) {
+            SurfaceHit hit;
+            if (march_segment(o2, d, i, g, s, span, &hit) && !(hit.distance <= 1e-9) &&
+                !(hit.distance >= span - 1e-9))
+              blocked = true;
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, blocked)) return false;
+    }
+    axis = w.advance(g);
+  }
+  return true;
+}
+
 }  // namespace pcr

@@ -197,15 +197,19 @@ std::vector<EP> dedup_by_label(std::vector<EP> paths) {
 }
 
 // dedup_by_fresnel (refine.cpp:345-372)
+// Kept paths are bucketed by (tx, rx, kind sequence): a path is only ever compared
+// with kept paths of its own bucket, visited in kept (= delay) order, which is the
+// reference's scan with the non-matching entries skipped.
 std::vector<EP> dedup_by_fresnel(std::vector<EP> paths, double freq) {
   const double lambda = kC / freq;
   sort_by_delay(paths);
   std::vector<EP> kept;
+  std::map<std::tuple<uint32_t, uint32_t, std::vector<int>>, std::vector<size_t>> buckets;
   for (EP& p : paths) {
     bool dup = false;
-    for (const EP& q : kept) {
-      if (q.tx_id != p.tx_id || q.rx_id != p.rx_id) continue;
-      if (kinds(q) != kinds(p)) continue;
+    auto& bucket = buckets[{p.tx_id, p.rx_id, kinds(p)}];
+    for (size_t qi : bucket) {
+      const EP& q = kept[qi];
       bool inside = true;
       for (size_t k = 0; k < p.its.size() && inside; ++k) {
         const V3 a = k == 0 ? q.tx : q.its[k - 1].pos;
@@ -218,7 +222,10 @@ std::vector<EP> dedup_by_fresnel(std::vector<EP> paths, double freq) {
         break;
       }
     }
-    if (!dup) kept.push_back(std::move(p));
+    if (!dup) {
+      bucket.push_back(kept.size());
+      kept.push_back(std::move(p));
+    }
   }
   return kept;
 }

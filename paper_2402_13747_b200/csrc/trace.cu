@@ -126,34 +126,53 @@ __global__ void materialize_kernel(const Node* __restrict__ nodes, uint32_t node
 // cannot produce output at this depth (non-RX at depth >= max_interactions,
 // edges once the diffraction budget is spent): the reference traces them and
 // discards the reception (tracer.cpp:441, 456), so the output is unchanged.
-__global__ void walk_kernel(const Ray* __restrict__ rays, uint32_t n_rays, GridView g, TraceCfg c, bool filter,
-                            Task* __restrict__ tasks, uint32_t* __restrict__ n_tasks, uint32_t cap,
-                            unsigned long long* __restrict__ stats) {
-  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per ray (warp_cone_walk); surviving IEs are appended with one atomic per
+// warp round.
+constexpr int kWalkThreads = 128;
+__global__ void __launch_bounds__(kWalkThreads) walk_kernel(const Ray* __restrict__ rays, uint32_t n_rays, GridView g,
+                                                            TraceCfg c, bool filter, Task* __restrict__ tasks,
+                                                            uint32_t* __restrict__ n_tasks, uint32_t cap,
+                                                            unsigned long long* __restrict__ stats) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const unsigned lt = (1u << lane) - 1u;
   uint32_t cells = 0, ies = 0;
-  if (k < n_rays) {
+  for (uint32_t k = warp; k < n_rays; k += nwarps) {
     const Ray r = rays[k];
-    if (r.alive) {
-      const bool can_refl = r.depth < c.max_interactions;
-      const bool can_diff = can_refl && r.dc < c.max_diffractions;
-      cone_walk(
-          g, r, [](uint32_t) {},
-          [&](uint32_t i) {
-            if (filter) {
-              const uint32_t kind = g.ie_meta[i] & 3u;
-              if (kind == kSurface && !can_refl) return;
-              if (kind == kEdge && !can_diff) return;
-            }
-            const uint32_t slot = atomic_append(n_tasks);
+    if (!r.alive) continue;
+    const bool can_refl = r.depth < c.max_interactions;
+    const bool can_diff = can_refl && r.dc < c.max_diffractions;
+    warp_cone_walk(
+        g, r, [](uint32_t) {},
+        [&](uint32_t i, bool pass) {
+          if (pass && filter) {
+            const uint32_t kind = g.ie_meta[i] & 3u;
+            if ((kind == kSurface && !can_refl) || (kind == kEdge && !can_diff)) pass = false;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, pass);
+          if (!m) return;
+          const int leader = __ffs(m) - 1;
+          uint32_t base = 0;
+          if (lane == leader) base = atomicAdd(n_tasks, static_cast<uint32_t>(__popc(m)));
+          base = __shfl_sync(0xffffffffu, base, leader);
+          if (pass) {
+            const uint32_t slot = base + __popc(m & lt);
             if (slot < cap) tasks[slot] = Task{k, i};
-          },
-          &cells, &ies);
-    }
+          }
+        },
+        &cells, &ies);
   }
-  if (stats) {
-    warp_add_u64(stats, cells);
-    warp_add_u64(stats + 1, ies);
+  if (stats && lane == 0) {
+    atomicAdd(stats, static_cast<unsigned long long>(cells));
+    atomicAdd(stats + 1, static_cast<unsigned long long>(ies));
   }
+}
+
+unsigned walk_blocks(uint64_t n_rays, int sm_count) {
+  const uint64_t want = (n_rays * 32 + kWalkThreads - 1) / kWalkThreads;
+  const uint64_t cap = static_cast<uint64_t>(sm_count) * 16;
+  return static_cast<unsigned>(want < cap ? (want ? want : 1) : cap);
 }
 
 struct SpawnOut {
@@ -165,17 +184,31 @@ struct SpawnOut {
 };
 
 // K13: visibility + hit + spawn.
-__global__ void visibility_kernel(const Task* __restrict__ tasks, uint32_t n_tasks, const Ray* __restrict__ rays,
-                                  const Node* __restrict__ parent_nodes, GridView g, SceneView s, TraceCfg c,
-                                  SpawnOut o) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_tasks) return;
-  const Task tk = tasks[t];
-  const Ray r = rays[tk.ray];
+// One warp per task: warp_segment_visible, then lane 0 computes the hit and spawns.
+__device__ void spawn_reception(const Task tk, const Ray& r, const Node* __restrict__ parent_nodes, const GridView& g,
+                                const SceneView& s, const TraceCfg& c, SpawnOut& o);
+
+__global__ void __launch_bounds__(128) visibility_kernel(const Task* __restrict__ tasks, uint32_t n_tasks,
+                                                         const Ray* __restrict__ rays,
+                                                         const Node* __restrict__ parent_nodes, GridView g,
+                                                         SceneView s, TraceCfg c, SpawnOut o) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t t = warp; t < n_tasks; t += nwarps) {
+    const Task tk = tasks[t];
+    const Ray r = rays[tk.ray];
+    const V3 rp = ld3(g.ie_rp[tk.ie]);
+    if (!warp_segment_visible(r.o, rp, tk.ie, g, s)) continue;
+    if (lane == 0) spawn_reception(tk, r, parent_nodes, g, s, c, o);
+  }
+}
+
+__device__ void spawn_reception(const Task tk, const Ray& r, const Node* __restrict__ parent_nodes, const GridView& g,
+                                const SceneView& s, const TraceCfg& c, SpawnOut& o) {
+  (void)c;
   const uint32_t i = tk.ie;
   const V3 rp = ld3(g.ie_rp[i]);
-  const bool vis = segment_visible(r.o, rp, i, g, s);
-  if (!vis) return;
   const uint32_t kind = g.ie_meta[i] & 3u;
   if (kind == kReceiver) {
     const uint32_t slot = atomic_append(o.n_cands);
@@ -237,16 +270,31 @@ struct TxOut {
   double* hinc;
 };
 
-__global__ void transmission_kernel(GridView g, SceneView s, V3 tx, TxOut o) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= g.n_ies) return;
-  o.los[i] = 0;
-  o.hit[i] = 0;
+__device__ void transmission_hit(uint32_t i, const V3& tx, const GridView& g, const SceneView& s, TxOut& o);
+
+// one warp per IE: warp_segment_visible, then lane 0 classifies the reception
+__global__ void __launch_bounds__(128) transmission_kernel(GridView g, SceneView s, V3 tx, TxOut o) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = warp; i < g.n_ies; i += nwarps) {
+    const V3 rp = ld3(g.ie_rp[i]);
+    const uint32_t kind = g.ie_meta[i] & 3u;
+    const V3 dir = safe_normalized(rp - tx);
+    bool go = !(is_zero(dir) && kind != kReceiver);
+    if (go) go = warp_segment_visible(tx, rp, i, g, s);
+    if (lane == 0) {
+      o.los[i] = 0;
+      o.hit[i] = 0;
+      if (go) transmission_hit(i, tx, g, s, o);
+    }
+  }
+}
+
+__device__ void transmission_hit(uint32_t i, const V3& tx, const GridView& g, const SceneView& s, TxOut& o) {
   const V3 rp = ld3(g.ie_rp[i]);
   const uint32_t kind = g.ie_meta[i] & 3u;
   const V3 dir = safe_normalized(rp - tx);
-  if (is_zero(dir) && kind != kReceiver) return;
-  if (!segment_visible(tx, rp, i, g, s)) return;
   if (kind == kReceiver) {
     o.los[i] = 1;
     return;
@@ -578,8 +626,17 @@ __global__ void reception_kernel(const Task* __restrict__ tasks, uint32_t n, con
 __global__ void segvis_kernel(const double* __restrict__ o, const double* __restrict__ tgt,
                               const uint32_t* __restrict__ tie, uint64_t n, GridView g, SceneView s,
                               uint8_t* __restrict__ out) {
-  const uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (k < n) out[k] = segment_visible(load3(o + 3 * k), load3(tgt + 3 * k), tie[k], g, s) ? 1 : 0;
+  // even segments through the warp-cooperative walk, odd ones through the per-thread
+  // walk (refinement's final check): both must agree with the reference
+  const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t k = 2 * warp; k < n; k += 2 * nwarps) {
+    const bool v = warp_segment_visible(load3(o + 3 * k), load3(tgt + 3 * k), tie[k], g, s);
+    if (lane == 0) out[k] = v ? 1 : 0;
+    if (lane == 1 && k + 1 < n)
+      out[k + 1] = segment_visible(load3(o + 3 * (k + 1)), load3(tgt + 3 * (k + 1)), tie[k + 1], g, s) ? 1 : 0;
+  }
 }
 
 unsigned nb(uint64_t n, unsigned t = kT) { return static_cast<unsigned>((n + t - 1) / t ? (n + t - 1) / t : 1); }
@@ -657,7 +714,7 @@ void transmission_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, u
     count_launch();
     {
       KTimer kt(ctx, "transmission");
-      transmission_kernel<<<nb(n, 128), 128, 0, s>>>(grid.view(), scene.view(), tx,
+      transmission_kernel<<<walk_blocks(n, ctx.sm_count), 128, 0, s>>>(grid.view(), scene.view(), tx,
                                                      TxOut{los.get(), hit.get(), hp.get(), hn.get(), hi.get()});
     }
     PCR_LAUNCH_CHECK();
@@ -868,7 +925,8 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
       count_launch();
       {
         KTimer kt(ctx, "cone_walk");
-        walk_kernel<<<nb(nr, 128), 128, 0, s>>>(rays.get(), nr, gv, c, true, tasks.get(), counters.get(),
+        walk_kernel<<<walk_blocks(nr, ctx.sm_count), kWalkThreads, 0, s>>>(rays.get(), nr, gv, c, true,
+                                                                            tasks.get(), counters.get(),
                                                 static_cast<uint32_t>(task_cap), walk_stats.get());
       }
       PCR_LAUNCH_CHECK();
@@ -903,7 +961,7 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
     count_launch();
     {
       KTimer kt(ctx, "visibility");
-      visibility_kernel<<<nb(n_tasks, 128), 128, 0, s>>>(
+      visibility_kernel<<<walk_blocks(n_tasks, ctx.sm_count), 128, 0, s>>>(
           tasks.get(), n_tasks, rays.get(), nodes.get(), gv, sv, c,
           SpawnOut{nodes.get(), counters.get(), cands.get(), counters.get() + 1, nullptr});
     }
@@ -1097,7 +1155,9 @@ void api_cone_trace_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, 
     PCR_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(uint32_t), s));
     if (n_rays) {
       count_launch();
-      walk_kernel<<<nb(n_rays, 128), 128, 0, s>>>(rays.get(), static_cast<uint32_t>(n_rays), gv, c, false,
+      walk_kernel<<<walk_blocks(n_rays, ctx.sm_count), kWalkThreads, 0, s>>>(rays.get(),
+                                                                              static_cast<uint32_t>(n_rays), gv, c,
+                                                                              false,
                                                   tasks.get(), cnt.get(), static_cast<uint32_t>(cap), nullptr);
       PCR_LAUNCH_CHECK();
     }
@@ -1215,7 +1275,8 @@ void api_segment_visible_batch(Ctx& ctx, const GridDev& grid, const SceneDev& sc
   h2d(t.get(), target, 3 * n, s);
   h2d(ti.get(), target_ie, n, s);
   count_launch();
-  segvis_kernel<<<nb(n, 128), 128, 0, s>>>(o.get(), t.get(), ti.get(), n, grid.view(), scene.view(), vis.get());
+  segvis_kernel<<<walk_blocks((n + 1) / 2, ctx.sm_count), 128, 0, s>>>(o.get(), t.get(), ti.get(), n, grid.view(),
+                                                                       scene.view(), vis.get());
   PCR_LAUNCH_CHECK();
   d2h(visible_out, vis.get(), n, s);
   PCR_CUDA(cudaStreamSynchronize(s));

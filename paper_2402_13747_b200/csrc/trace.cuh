@@ -142,6 +142,157 @@ __device__ __forceinline__ void cone_walk(const GridView& g, const Ray& r, OnEva
   if (n_ies) *n_ies += ies_seen;
 }
 
+// cone_intersects_sphere (tracer.cpp:129-136) with an exact-equivalent fast path.
+// beta = atan2(|vc x d|, vc.d) <= rhs = alpha + asin(min(1, r/dist)) is, on [0, pi],
+// cos(beta) >= cos(rhs) with cos(beta) = vc.d / (|vc||d|) and
+// cos(rhs) = cos(alpha) sqrt((1-s)(1+s)) - sin(alpha) s. Both sides are evaluated to
+// ~1e-15; libm's atan2/asin are within a few ulp; so whenever the cosines differ by
+// more than 1e-9 the reference's comparison has the same outcome, and only the rare
+// knife edge inside that band pays for the transcendental evaluation. alpha < 1 rad
+// keeps rhs < pi (the reference's default half-angle is 0.5 deg).
+struct ConeConsts {
+  double alpha, ca, sa, dnorm;
+  bool fast;
+};
+__device__ __forceinline__ ConeConsts cone_consts(double alpha, const V3& d) {
+  ConeConsts k;
+  k.alpha = alpha;
+  k.ca = cos(alpha);
+  k.sa = sin(alpha);
+  k.dnorm = norm(d);
+  k.fast = alpha >= 0.0 && alpha < 1.0 && k.dnorm > 0.0;
+  return k;
+}
+__device__ __forceinline__ bool cone_test(const V3& o, const V3& d, const ConeConsts& k, const V3& c, double r) {
+  const V3 vc = c - o;
+  const double dist = norm(vc);
+  if (dist <= r) return true;
+  if (k.fast) {
+    const double s = smin(1.0, r / dist);
+    const double cb = dot(vc, d) / (dist * k.dnorm);
+    const double cr = k.ca * sqrt((1.0 - s) * (1.0 + s)) - k.sa * s;
+    const double diff = cb - cr;
+    if (diff > 1e-9) return true;
+    if (diff < -1e-9) return false;
+  }
+  const double beta = angle_between(vc, d);
+  return beta <= k.alpha + asin(smin(1.0, r / dist));
+}
+
+// Warp-cooperative voxel_cone_trace walk: the 32 lanes hold the same ray, walker
+// and dedup ring (warp-uniform control flow); at an evaluating voxel lane l < 27
+// takes neighbour l (z -> y -> x order as in tracer.cpp:339-341), and the IEs of
+// the cells that pass the voxel cone test are flattened across lanes in rounds of
+// 32. on_ie(i, pass) is called by every lane each round (pass = the IE survived the
+// self-exclusion / cone / plane / coincidence tests), so it may use warp
+// collectives. Same evaluated set and same surviving IEs as cone_walk.
+template <typename OnEval, typename OnIE>
+__device__ __forceinline__ void warp_cone_walk(const GridView& g, const Ray& r, OnEval on_eval, OnIE on_ie,
+                                               uint32_t* n_cells = nullptr, uint32_t* n_ies = nullptr) {
+  if (g.n_ies == 0) return;
+  const int lane = threadIdx.x & 31;
+  const double half_angle = 0.5 * r.apex;
+  const double exempt_radius = 2.0 * g.sub_radius;
+  const ConeConsts kc = cone_consts(half_angle, r.d);
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  const int ox = lane % 3 - 1, oy = (lane / 3) % 3 - 1, oz = lane / 9 - 1;
+  int ring[8][3];
+  int ring_n = 0;
+  uint32_t cells_seen = 0, ies_seen = 0;
+  Walker w;
+  w.init(g, r.o, r.d, 0.0, inf);
+  while (w.active) {
+    const int4 here = g.cells[linear_index(g, w.v[0], w.v[1], w.v[2])];
+    const int march = here.z;
+    if (here.x != here.y || march <= 1) {
+      const int nx = w.v[0] + ox, ny = w.v[1] + oy, nz = w.v[2] + oz;
+      bool valid = lane < 27 && in_bounds(g, nx, ny, nz);
+      for (int k = 0; k < ring_n && valid; ++k)
+        if (abs(nx - ring[k][0]) <= 1 && abs(ny - ring[k][1]) <= 1 && abs(nz - ring[k][2]) <= 1) valid = false;
+      int b = 0, cnt = 0;
+      if (valid) {
+        const uint32_t ni = linear_index(g, nx, ny, nz);
+        on_eval(ni);
+        const int4 cell = g.cells[ni];
+        if (cell.x != cell.y && cone_test(r.o, r.d, kc, voxel_center(g, nx, ny, nz), g.voxel_radius)) {
+          b = cell.x;
+          cnt = cell.y - cell.x;
+        }
+      }
+      cells_seen += __popc(__ballot_sync(0xffffffffu, valid));
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      ies_seen += static_cast<uint32_t>(total);
+      for (int base = 0; base < total; base += 32) {
+        const int f = base + lane;
+        int jlo = 0, jhi = 31;  // owning lane: first j with incl_j > f
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+          const int mid = (jlo + jhi) >> 1;
+          const int v = __shfl_sync(0xffffffffu, incl, mid);
+          if (v > f) jhi = mid;
+          else jlo = mid + 1;
+        }
+        const int cb = __shfl_sync(0xffffffffu, b, jlo);
+        const int ce = __shfl_sync(0xffffffffu, incl - cnt, jlo);
+        bool pass = false;
+        uint32_t i = 0;
+        if (f < total) {
+          i = static_cast<uint32_t>(cb + (f - ce));
+          pass = i != r.origin_ie;
+          if (pass) {
+            const double4 sc4 = g.ie_sc[i];
+            const V3 sc = ld3(sc4);
+            if (r.origin_ie != kNoIe && g.ie_label[i] == r.origin_label && norm(sc - r.o) <= exempt_radius)
+              pass = false;
+            else if (!cone_test(r.o, r.d, kc, sc, sc4.w))
+              pass = false;
+            else {
+              const V3 rp = ld3(g.ie_rp[i]);
+              if (!passes_planes(r, rp) || norm(rp - r.o) < kTiny) pass = false;
+            }
+          }
+        }
+        on_ie(i, pass);
+      }
+      // dedup ring: keep earlier evaluating voxels within Chebyshev distance 2
+      int m = 0;
+      for (int k = 0; k < ring_n; ++k) {
+        if (abs(w.v[0] - ring[k][0]) <= 2 && abs(w.v[1] - ring[k][1]) <= 2 && abs(w.v[2] - ring[k][2]) <= 2) {
+          ring[m][0] = ring[k][0];
+          ring[m][1] = ring[k][1];
+          ring[m][2] = ring[k][2];
+          ++m;
+        }
+      }
+      if (m == 8) {
+        for (int k = 0; k < 7; ++k) {
+          ring[k][0] = ring[k + 1][0];
+          ring[k][1] = ring[k + 1][1];
+          ring[k][2] = ring[k + 1][2];
+        }
+        m = 7;
+      }
+      ring[m][0] = w.v[0];
+      ring[m][1] = w.v[1];
+      ring[m][2] = w.v[2];
+      ring_n = m + 1;
+    }
+    if (march >= 2) {
+      w.init(g, r.o, r.d, w.t_entry + static_cast<double>(march - 1) * g.voxel_size, inf);
+    } else {
+      w.advance(g);
+    }
+  }
+  if (n_cells) *n_cells += cells_seen;
+  if (n_ies) *n_ies += ies_seen;
+}
+
 // Warp-aggregated 64-bit counter add.
 __device__ __forceinline__ void warp_add_u64(unsigned long long* dst, unsigned long long v) {
 #pragma unroll
