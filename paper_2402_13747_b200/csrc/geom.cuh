@@ -83,8 +83,8 @@ struct SurfaceEstimate {
 
 // estimate_surface (surface.cpp:24-62). Non-planar payloads only; exp() is CUDA's
 // (<= 1 ulp from glibc's).
-__device__ inline SurfaceEstimate estimate_surface(const V3& x, uint32_t ie, const GridView& g,
-                                                   const SceneView& s) {
+static __device__ __noinline__ SurfaceEstimate estimate_surface(const V3& x, uint32_t ie, const GridView& g,
+                                                                const SceneView& s) {
   const double h = g.sub_edge;
   const double inv_h2 = 1.0 / (h * h);
   V3 p_sum{0, 0, 0}, n_sum{0, 0, 0};
@@ -128,9 +128,14 @@ __device__ __forceinline__ double sdf_value_at(const V3& x, uint32_t ie, bool pl
   return estimate_surface(x, ie, g, s).sdf;
 }
 
-// march_segment (surface.cpp:64-134); returns false for std::nullopt.
-__device__ inline bool march_segment(const V3& origin, const V3& dir, uint32_t ie, const GridView& g,
-                                     const SceneView& s, double t_max, SurfaceHit* out) {
+static __device__ __noinline__ bool march_window(const V3& origin, const V3& dir, uint32_t ie, const GridView& g,
+                                                 const SceneView& s, double t_lo, double t_hi, SurfaceHit* out);
+
+// march_segment (surface.cpp:64-134); returns false for std::nullopt. The planar
+// route (the only one the rectangle scenes take) is inlined; sphere tracing over the
+// Gaussian SDF lives out of line in march_window.
+__device__ __forceinline__ bool march_segment(const V3& origin, const V3& dir, uint32_t ie, const GridView& g,
+                                              const SceneView& s, double t_max, SurfaceHit* out) {
   const double eps = g.hit_eps;
   const double4 sc4 = g.ie_sc[ie];
   const V3 sc = ld3(sc4);
@@ -139,7 +144,34 @@ __device__ inline bool march_segment(const V3& origin, const V3& dir, uint32_t i
   const double t_lo = smax(0.0, t_center - r);
   const double t_hi = smin(t_center + r, t_max);
   if (t_hi <= t_lo) return false;
+  if (!ie_planar(g, ie)) return march_window(origin, dir, ie, g, s, t_lo, t_hi, out);
+  const double4 pp4 = g.ie_pp[ie], pn4 = g.ie_pn[ie];
+  const V3 pp = ld3(pp4), pn = ld3(pn4);
+  auto make_hit = [&](double t) {
+    const double dn = dot(dir, pn);
+    if (fabs(dn) > 1e-12) {
+      const double t_star = dot(pp - origin, pn) / dn;
+      if (t_star >= t_lo && t_star <= t_hi) t = t_star;
+    }
+    if (out) {
+      out->position = origin + t * dir;
+      out->normal = pn;
+      out->label = g.ie_label[ie];
+      out->distance = t;
+    }
+    return true;
+  };
+  const double f = dot((origin + t_lo * dir) - pp, pn);
+  if (fabs(f) <= eps) return make_hit(t_lo);
+  const double f_hi = dot((origin + t_hi * dir) - pp, pn);
+  if (f * f_hi < 0.0) return make_hit(0.5 * (t_lo + t_hi));
+  if (fabs(f_hi) <= eps) return make_hit(t_hi);
+  return false;
+}
 
+static __device__ __noinline__ bool march_window(const V3& origin, const V3& dir, uint32_t ie, const GridView& g,
+                                                 const SceneView& s, double t_lo, double t_hi, SurfaceHit* out) {
+  const double eps = g.hit_eps;
   const bool planar = ie_planar(g, ie);
   V3 pp{0, 0, 0}, pn{0, 0, 1};
   if (planar) {

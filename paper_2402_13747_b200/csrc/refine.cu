@@ -220,10 +220,25 @@ __device__ __forceinline__ bool same_snapshot(const Snapshot& sn, const RNode* n
   return true;
 }
 
-__global__ void __launch_bounds__(128) refine_kernel(CandIn in, uint32_t n, GridView g, SceneView s, double delta,
-                                                     int rho, double step_size, RefOut o) {
-  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
+__device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const GridView& g, const SceneView& s,
+                                           double delta, int rho, double step_size, const RefOut& o);
+
+// Persistent threads with per-thread work stealing: iteration counts range from 1 to
+// rho, so a thread that finishes a path takes the next one instead of idling until
+// the slowest lane of its warp is done.
+constexpr int kRefineThreads = 128;
+__global__ void __launch_bounds__(kRefineThreads, 4) refine_kernel(CandIn in, uint32_t n, GridView g, SceneView s,
+                                                                   double delta, int rho, double step_size, RefOut o,
+                                                                   uint32_t* next_cand) {
+  for (;;) {
+    const uint32_t k = atomicAdd(next_cand, 1u);
+    if (k >= n) break;
+    refine_one(k, in, g, s, delta, rho, step_size, o);
+  }
+}
+
+__device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const GridView& g, const SceneView& s,
+                                           double delta, int rho, double step_size, const RefOut& o) {
   const int d = static_cast<int>(in.n_inter[k]);
   const V3 tx = load3(in.tx + 3ull * k), rx = load3(in.rx + 3ull * k);
   o.has_path[k] = 0;
@@ -429,14 +444,21 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
   if (!in.n) return;
   CandIn ci{in.stride, in.tx, in.rx, in.n_inter, in.kind, in.pos, in.label, in.nrm, in.edge, in.coarse_length};
   DBuf<unsigned long long> stats(2, s);
+  DBuf<uint32_t> next(1, s);
+  PCR_CUDA(cudaMemsetAsync(next.get(), 0, sizeof(uint32_t), s));
   PCR_CUDA(cudaMemsetAsync(stats.get(), 0, 2 * sizeof(unsigned long long), s));
   RefOut ro{out.reason.get(), out.has_path.get(), out.pos.get(), out.nrm.get(), out.label.get(),
             out.length.get(), out.delay.get(), out.gnorm.get(), out.iters.get(), stats.get()};
   count_launch();
   {
     KTimer kt(ctx, "refine");
-    refine_kernel<<<nb(in.n, 128), 128, 0, s>>>(ci, in.n, grid.view(), scene.view(), p.delta, p.rho, p.step_size,
-                                                ro);
+    // enough resident threads to fill every SM at the kernel's occupancy
+    int per_sm = 0;
+    PCR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, kRefineThreads, 0));
+    const uint64_t want = (static_cast<uint64_t>(in.n) + kRefineThreads - 1) / kRefineThreads;
+    const uint64_t cap = static_cast<uint64_t>(ctx.sm_count) * (per_sm > 0 ? per_sm : 1);
+    refine_kernel<<<static_cast<unsigned>(want < cap ? want : cap), kRefineThreads, 0, s>>>(
+        ci, in.n, grid.view(), scene.view(), p.delta, p.rho, p.step_size, ro, next.get());
   }
   PCR_LAUNCH_CHECK();
   unsigned long long hs[2];

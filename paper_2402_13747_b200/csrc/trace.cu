@@ -188,7 +188,7 @@ struct SpawnOut {
 __device__ void spawn_reception(const Task tk, const Ray& r, const Node* __restrict__ parent_nodes, const GridView& g,
                                 const SceneView& s, const TraceCfg& c, SpawnOut& o);
 
-__global__ void __launch_bounds__(128) visibility_kernel(const Task* __restrict__ tasks, uint32_t n_tasks,
+__global__ void __launch_bounds__(128, 6) visibility_kernel(const Task* __restrict__ tasks, uint32_t n_tasks,
                                                          const Ray* __restrict__ rays,
                                                          const Node* __restrict__ parent_nodes, GridView g,
                                                          SceneView s, TraceCfg c, SpawnOut o) {
@@ -273,7 +273,7 @@ struct TxOut {
 __device__ void transmission_hit(uint32_t i, const V3& tx, const GridView& g, const SceneView& s, TxOut& o);
 
 // one warp per IE: warp_segment_visible, then lane 0 classifies the reception
-__global__ void __launch_bounds__(128) transmission_kernel(GridView g, SceneView s, V3 tx, TxOut o) {
+__global__ void __launch_bounds__(128, 4) transmission_kernel(GridView g, SceneView s, V3 tx, TxOut o) {
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;

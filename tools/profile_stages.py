@@ -40,7 +40,7 @@ def main():
     kt = pcray.kernel_times()
     pcray.set_profiling(False)
     out = {k: s[k] for k in ["ie_count", "grid_dims", "coarse_paths", "refined_paths", "rejected", "exact_paths",
-                             "transmission_rays", "cone_traces", "visibility_tests", "refine_iterations"]}
+                             "transmission_rays", "cone_traces", "visibility_tests", "refine_iterations", "refine_trials", "refine_marches", "walk_cells", "walk_ies"]}
     print(json.dumps(out))
     tot = sum(v[0] for v in kt.values())
     for k, (ms, n) in sorted(kt.items(), key=lambda kv: -kv[1][0]):
