@@ -124,3 +124,18 @@ def test_reference_unit_suites(oracle):
                        ("tracer", "box room propagation covers all six first-order reflections"),
                        ("tracer", "screen edge: diffraction is the only route around the occluder")], failing
     assert failed == 3
+
+
+@pytest.mark.parametrize("name", ["single_point", "two_labels", "edge_clip", "reception_points", "partition",
+                                  "determinism", "oblique_edge", "dup_rx_ids", "box_room", "nonplanar_patch"])
+def test_restated_voxelization_matches_reference(oracle, name):
+    """oracle/restate_vox.py (numpy restatement) == the compiled reference, bit for bit."""
+    from conftest import assert_grid_equal
+    from fixtures import voxel_grid_scenes
+    from oracle import restate_vox
+
+    scene = voxel_grid_scenes()[name]
+    for vs, dv in [(0.5, 2), (0.25, 1), (0.7, 3)]:
+        ref = oracle.build_grid(oracle.RefScene(scene), abi.voxel_params(vs, dv)).to_dict()
+        got = restate_vox.build_grid(scene, vs, dv)
+        assert_grid_equal(got, ref)
