@@ -291,6 +291,38 @@ int pcr_run_pipeline_on_scene(pcr_ctx* ctx, const pcr_scene_desc* scene,
 int pcr_run_pipeline_device(pcr_ctx* ctx, const pcr_scene* scene, const pcr_run_config* config,
                             pcr_summary** out);
 
+/* ---- sharded pipeline: one process per GPU ----------------------------- */
+/* run_pipeline_on_scene split across n_shards contexts (one per GPU). The reference
+ * parallelises the same loop over initial hits (tracer.cpp:476-533, parallel_for) and
+ * refines candidates independently (pipeline.cpp:148-187); the split is exact:
+ *   1. pcr_shard_trace: validate + build_grid + transmission_phase (full, on every
+ *      shard), then propagate over the initial hits t = shard (mod n_shards) of every
+ *      TX with this shard's own first-kappa (a superset of its share of the global
+ *      one). Rows: n_rows records of row_bytes (DFS key, group hash, candidate).
+ *   2. pcr_shard_rows copies them into caller device memory; the caller all-gathers
+ *      every shard's rows (e.g. an NCCL all-gather of a byte tensor).
+ *   3. pcr_shard_refine: global kappa over all rows (any concatenation order) -> the
+ *      reference's candidate list, identical on every shard; refine candidates
+ *      i = shard (mod n_shards). pcr_shard_outcomes copies the n_out outcome rows.
+ *   4. pcr_shard_stats returns this shard's work counters; the caller sums them over
+ *      shards and gathers every shard's outcome rows to one shard, whose
+ *      pcr_shard_finish produces the RunSummary of the unsharded run (same counts,
+ *      same exact paths in the same order; timings are this shard's).
+ * Device pointers are in the context's device memory; rows are plain bytes. */
+typedef struct pcr_shard_stats {
+  uint64_t cone_traces, visibility_tests, walk_cells, walk_ies; /* propagation of the shard */
+  uint64_t refine_iterations, refine_trials, refine_marches;    /* refinement of the shard */
+} pcr_shard_stats;
+int pcr_shard_trace(pcr_ctx* ctx, const pcr_scene* scene, const pcr_run_config* config, uint32_t shard,
+                    uint32_t n_shards, uint64_t* n_rows, uint64_t* row_bytes);
+int pcr_shard_rows(pcr_ctx* ctx, void* dst_device);
+int pcr_shard_refine(pcr_ctx* ctx, const pcr_scene* scene, const void* rows_device, uint64_t n_rows,
+                     uint64_t* n_out, uint64_t* out_row_bytes);
+int pcr_shard_outcomes(pcr_ctx* ctx, void* dst_device);
+int pcr_shard_stats_get(pcr_ctx* ctx, pcr_shard_stats* out);
+int pcr_shard_finish(pcr_ctx* ctx, const void* outcome_rows_device, uint64_t n_rows,
+                     const pcr_shard_stats* totals, pcr_summary** out);
+
 /* ---- instrumentation (no reference counterpart) ------------------------------------ */
 /* cudaStream_t the context launches on, as an opaque pointer (for caller-side events) */
 void* pcr_stream(pcr_ctx* ctx);

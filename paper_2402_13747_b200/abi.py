@@ -104,6 +104,15 @@ class Summary(C.Structure):
     ]
 
 
+SHARD_STATS_FIELDS = ("cone_traces", "visibility_tests", "walk_cells", "walk_ies", "refine_iterations",
+                      "refine_trials", "refine_marches")
+
+
+class ShardStats(C.Structure):
+    """pcr_shard_stats: one shard's work counters (summed over shards by the caller)."""
+    _fields_ = [(f, C.c_uint64) for f in SHARD_STATS_FIELDS]
+
+
 class RayDesc(C.Structure):
     _fields_ = [
         ("origin", C.c_double * 3), ("direction", C.c_double * 3), ("apex_angle", C.c_double),

@@ -74,6 +74,7 @@ void pcr_destroy(pcr_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
   ctx->c.fan_table.release();
+  ctx->c.shard.reset();  // its buffers are freed on the context's stream
   cudaStreamSynchronize(ctx->c.stream);
   cudaStreamDestroy(ctx->c.stream);
   delete ctx;
@@ -343,6 +344,46 @@ int pcr_run_pipeline_device(pcr_ctx* ctx, const pcr_scene* scene, const pcr_run_
   return guarded(ctx, [&] {
     if (!scene || !config || !out) throw pcr::Error(PCR_ERR_INVALID, "null argument");
     pcr::api_run_pipeline_device(ctx->c, scene->s, *config, out);
+  });
+}
+
+int pcr_shard_trace(pcr_ctx* ctx, const pcr_scene* scene, const pcr_run_config* config, uint32_t shard,
+                    uint32_t n_shards, uint64_t* n_rows, uint64_t* row_bytes) {
+  return guarded(ctx, [&] {
+    if (!scene || !config || !n_rows || !row_bytes) throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    pcr::api_shard_trace(ctx->c, scene->s, *config, shard, n_shards, n_rows, row_bytes);
+  });
+}
+
+int pcr_shard_rows(pcr_ctx* ctx, void* dst_device) {
+  return guarded(ctx, [&] { pcr::api_shard_rows(ctx->c, dst_device); });
+}
+
+int pcr_shard_refine(pcr_ctx* ctx, const pcr_scene* scene, const void* rows_device, uint64_t n_rows,
+                     uint64_t* n_out, uint64_t* out_row_bytes) {
+  return guarded(ctx, [&] {
+    if (!scene || !n_out || !out_row_bytes || (n_rows && !rows_device))
+      throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    pcr::api_shard_refine(ctx->c, scene->s, rows_device, n_rows, n_out, out_row_bytes);
+  });
+}
+
+int pcr_shard_outcomes(pcr_ctx* ctx, void* dst_device) {
+  return guarded(ctx, [&] { pcr::api_shard_outcomes(ctx->c, dst_device); });
+}
+
+int pcr_shard_stats_get(pcr_ctx* ctx, pcr_shard_stats* out) {
+  return guarded(ctx, [&] {
+    if (!out) throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    pcr::api_shard_stats(ctx->c, out);
+  });
+}
+
+int pcr_shard_finish(pcr_ctx* ctx, const void* outcome_rows_device, uint64_t n_rows, const pcr_shard_stats* totals,
+                     pcr_summary** out) {
+  return guarded(ctx, [&] {
+    if (!totals || !out || (n_rows && !outcome_rows_device)) throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    pcr::api_shard_finish(ctx->c, outcome_rows_device, n_rows, *totals, out);
   });
 }
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -116,8 +117,11 @@ struct GridDev {
   }
 };
 
+struct ShardState;  // pipeline.cu: state between the pcr_shard_* calls
+
 struct Ctx {
   int device = 0;
+  std::shared_ptr<ShardState> shard;
   cudaStream_t stream = nullptr;
   std::string last_error;
   std::mutex mu;

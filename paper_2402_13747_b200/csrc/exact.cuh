@@ -53,6 +53,17 @@ PCR_HD bool operator!=(const V3& a, const V3& b) { return !(a == b); }
 PCR_HD double dot(const V3& a, const V3& b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
 PCR_HD double sqnorm(const V3& a) { return dot(a, a); }
 PCR_HD double norm(const V3& a) { return sqrt(sqnorm(a)); }
+// norm(v) <= y for y > 0, decided on the squared norm when it is clear of the rounding
+// band: a <= y²(1-1e-12) implies sqrt_rn(a) < y and a >= y²(1+1e-12) implies
+// sqrt_rn(a) > y (each rounding is within 2^-53 relative); the sqrt runs only inside
+// the band, so the result equals the reference's `v.norm() <= y` bit for bit.
+PCR_HD bool norm_le(const V3& v, double y) {
+  const double a = sqnorm(v);
+  const double yy = y * y;
+  if (a <= yy * (1.0 - 1e-12)) return true;
+  if (a >= yy * (1.0 + 1e-12)) return false;
+  return sqrt(a) <= y;
+}
 PCR_HD V3 normalized(const V3& v) {
   const double z = sqnorm(v);
   return z > 0.0 ? v / sqrt(z) : v;

@@ -131,6 +131,38 @@ __device__ __forceinline__ double sdf_value_at(const V3& x, uint32_t ie, bool pl
 static __device__ __noinline__ bool march_window(const V3& origin, const V3& dir, uint32_t ie, const GridView& g,
                                                  const SceneView& s, double t_lo, double t_hi, SurfaceHit* out);
 
+// march_segment's planar branch (surface.cpp:74-106) on the window [t_lo, t_hi]:
+// endpoint / sign test, then the exact snap t* = (pp-o)·n / (d·n) when it falls in
+// the window. Returns the hit distance only (the record is o + t·d, the plane normal
+// and the IE label), false for std::nullopt.
+__device__ __forceinline__ bool planar_march_t(const V3& origin, const V3& dir, uint32_t ie, const GridView& g,
+                                               double t_lo, double t_hi, double& t) {
+  if (t_hi <= t_lo) return false;
+  const double eps = g.hit_eps;
+  const double4 pp4 = g.ie_pp[ie], pn4 = g.ie_pn[ie];
+  const V3 pp = ld3(pp4), pn = ld3(pn4);
+  double tc;
+  const double f = dot((origin + t_lo * dir) - pp, pn);
+  if (fabs(f) <= eps) {
+    tc = t_lo;
+  } else {
+    const double f_hi = dot((origin + t_hi * dir) - pp, pn);
+    if (f * f_hi < 0.0)
+      tc = 0.5 * (t_lo + t_hi);
+    else if (fabs(f_hi) <= eps)
+      tc = t_hi;
+    else
+      return false;
+  }
+  const double dn = dot(dir, pn);
+  if (fabs(dn) > 1e-12) {
+    const double t_star = dot(pp - origin, pn) / dn;
+    if (t_star >= t_lo && t_star <= t_hi) tc = t_star;
+  }
+  t = tc;
+  return true;
+}
+
 // march_segment (surface.cpp:64-134); returns false for std::nullopt. The planar
 // route (the only one the rectangle scenes take) is inlined; sphere tracing over the
 // Gaussian SDF lives out of line in march_window.
@@ -145,28 +177,15 @@ __device__ __forceinline__ bool march_segment(const V3& origin, const V3& dir, u
   const double t_hi = smin(t_center + r, t_max);
   if (t_hi <= t_lo) return false;
   if (!ie_planar(g, ie)) return march_window(origin, dir, ie, g, s, t_lo, t_hi, out);
-  const double4 pp4 = g.ie_pp[ie], pn4 = g.ie_pn[ie];
-  const V3 pp = ld3(pp4), pn = ld3(pn4);
-  auto make_hit = [&](double t) {
-    const double dn = dot(dir, pn);
-    if (fabs(dn) > 1e-12) {
-      const double t_star = dot(pp - origin, pn) / dn;
-      if (t_star >= t_lo && t_star <= t_hi) t = t_star;
-    }
-    if (out) {
-      out->position = origin + t * dir;
-      out->normal = pn;
-      out->label = g.ie_label[ie];
-      out->distance = t;
-    }
-    return true;
-  };
-  const double f = dot((origin + t_lo * dir) - pp, pn);
-  if (fabs(f) <= eps) return make_hit(t_lo);
-  const double f_hi = dot((origin + t_hi * dir) - pp, pn);
-  if (f * f_hi < 0.0) return make_hit(0.5 * (t_lo + t_hi));
-  if (fabs(f_hi) <= eps) return make_hit(t_hi);
-  return false;
+  double t;
+  if (!planar_march_t(origin, dir, ie, g, t_lo, t_hi, t)) return false;
+  if (out) {  // make_hit (surface.cpp:98-106)
+    out->position = origin + t * dir;
+    out->normal = ld3(g.ie_pn[ie]);
+    out->label = g.ie_label[ie];
+    out->distance = t;
+  }
+  return true;
 }
 
 static __device__ __noinline__ bool march_window(const V3& origin, const V3& dir, uint32_t ie, const GridView& g,

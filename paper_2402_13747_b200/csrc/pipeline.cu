@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <string>
 #include <tuple>
 #include <unordered_set>
@@ -16,6 +17,7 @@
 
 #include "host_alloc.hpp"
 #include "pipeline.hpp"
+#include "shard_rows.cuh"
 #include "stages.cuh"
 #include "trace.cuh"
 
@@ -370,211 +372,237 @@ void api_run_pipeline_device(Ctx& ctx, const SceneDev& scene, const pcr_run_conf
   run_pipeline_core(ctx, scene, cfg, out, 0.0);
 }
 
-void run_pipeline_core(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, pcr_summary** out,
-                       double upload_seconds) {
-  cudaStream_t s = ctx.stream;
-  pcr_summary* S = halloc<pcr_summary>(1);
-  auto fail = [&](const char* stage, const std::exception& e) {
-    std::free(S);
-    const Error* pe = dynamic_cast<const Error*>(&e);
-    std::string msg = e.what();
-    // device stages already prefix "trace: " style messages for their own errors
-    if (msg.rfind(std::string(stage) + ": ", 0) != 0) msg = std::string(stage) + ": " + msg;
-    throw Error(pe ? pe->code : PCR_ERR_RUNTIME, msg);
-  };
-  auto timing = [&](const char* name, double sec) {
+namespace {
+
+// One pipeline run's summary under construction (stage timings in reference order).
+struct Run {
+  pcr_summary* S;
+  explicit Run(pcr_summary* s) : S(s) {}
+  explicit Run(const pcr_run_config& cfg, const SceneDev& scene) : S(halloc<pcr_summary>(1)) {
+    S->hash = config_hash(cfg);
+    S->point_count = scene.n_points;
+    S->edge_count = scene.n_edges;
+  }
+  ~Run() { std::free(S); }
+  pcr_summary* release() {
+    pcr_summary* r = S;
+    S = nullptr;
+    return r;
+  }
+  void timing(const char* name, double sec) {
     if (S->n_timings < PCR_MAX_STAGES) {
       std::snprintf(S->timing_stage[S->n_timings], 16, "%s", name);
       S->timing_seconds[S->n_timings++] = sec;
     }
-  };
-  S->hash = config_hash(cfg);
-  S->point_count = scene.n_points;
-  S->edge_count = scene.n_edges;
-  const uint32_t n_tx = static_cast<uint32_t>(scene.h_tx_id.size());
-
-  auto t0 = Clock::now();
-  {
-    Violation v;
-    bool bad = false;
-    try {
-      bad = first_violation_device(ctx, scene, v);
-    } catch (const std::exception& e) {
-      fail("validate", e);
-    }
-    if (bad) {
-      std::free(S);
-      throw Error(PCR_ERR_RUNTIME, "validate: " + v.rule + " (" + v.detail + ")");
-    }
   }
-  timing("validate", since(t0) + upload_seconds);
+};
 
-  t0 = Clock::now();
-  GridDev grid;
+// Rethrow a stage failure with the reference's "stage: " prefix (pipeline.cpp:30-32).
+[[noreturn]] void stage_fail(const char* stage, const std::exception& e) {
+  const Error* pe = dynamic_cast<const Error*>(&e);
+  std::string msg = e.what();
+  // device stages already prefix "trace: " style messages for their own errors
+  if (msg.rfind(std::string(stage) + ": ", 0) != 0) msg = std::string(stage) + ": " + msg;
+  throw Error(pe ? pe->code : PCR_ERR_RUNTIME, msg);
+}
+
+void stage_validate(Ctx& ctx, const SceneDev& scene) {
+  Violation v;
+  bool bad = false;
+  try {
+    bad = first_violation_device(ctx, scene, v);
+  } catch (const std::exception& e) {
+    stage_fail("validate", e);
+  }
+  if (bad) throw Error(PCR_ERR_RUNTIME, "validate: " + v.rule + " (" + v.detail + ")");
+}
+
+void stage_voxelize(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, GridDev& grid, pcr_summary* S) {
   try {
     KTimer kt(ctx, "build_grid");
     build_grid_device(ctx, scene, cfg.voxel_size_m, cfg.division_factor, uint64_t(1) << 27, grid);
   } catch (const std::exception& e) {
-    fail("voxelize", e);
+    stage_fail("voxelize", e);
   }
   S->ie_count = grid.n_ies;
   for (int a = 0; a < 3; ++a) S->grid_dims[a] = grid.dims[a];
-  timing("voxelize", since(t0));
+}
 
-  // trace
-  t0 = Clock::now();
+pcr_trace_params trace_params_of(const pcr_run_config& cfg) {
   pcr_trace_params tp;
   tp.max_interactions = cfg.max_interactions;
   tp.kappa = cfg.kappa;
   tp.cone_apex_angle = cfg.cone_apex_angle_deg * 3.141592653589793238462643383279502884 / 180.0;
   tp.diffraction_ray_count = cfg.diffraction_ray_count;
   tp.max_diffractions = cfg.max_diffractions;
-  const uint32_t stride = static_cast<uint32_t>(std::max(1, cfg.max_interactions));
-  CandSet cs;
-  cs.stride = stride;
-  try {
-    std::vector<TxDev> txs(n_tx);
-    std::vector<CandDev> props(n_tx);
-    TraceStats st;
-    uint64_t total = 0;
-    for (uint32_t t = 0; t < n_tx; ++t) {
-      transmission_device(ctx, grid, scene, t, txs[t]);
-      propagate_device(ctx, grid, scene, t, txs[t].hit_ie.get(), txs[t].hit_kind.get(), txs[t].hit_pos.get(),
-                       txs[t].hit_nrm.get(), txs[t].hit_inc.get(), txs[t].n_hits, tp, props[t], st);
-      txs[t].hit_ie.release();
-      txs[t].hit_kind.release();
-      txs[t].hit_pos.release();
-      txs[t].hit_nrm.release();
-      txs[t].hit_inc.release();
-      total += txs[t].n_los + props[t].n;
-      S->transmission_rays += grid.n_ies;
-      S->visibility_tests += grid.n_ies;
-    }
-    S->cone_traces = st.cone_traces;
-    S->walk_cells = st.walk_cells;
-    S->walk_ies = st.walk_ies;
-    S->visibility_tests += st.visibility_tests;
-    if (total > 0xffffffffull) throw Error(PCR_ERR_NOMEM, "too many candidates");
-    cs.n = static_cast<uint32_t>(total);
-    const size_t m = total ? total : 1, ms = m * stride;
-    cs.tx_id.alloc(m, s);
-    cs.rx_id.alloc(m, s);
-    cs.n_inter.alloc(m, s);
-    cs.label.alloc(ms, s);
-    cs.ie.alloc(ms, s);
-    cs.edge.alloc(ms, s);
-    cs.kind.alloc(ms, s);
-    cs.tx_pos.alloc(3 * m, s);
-    cs.rx_pos.alloc(3 * m, s);
-    cs.length.alloc(m, s);
-    cs.pos.alloc(3 * ms, s);
-    cs.nrm.alloc(3 * ms, s);
-    PCR_CUDA(cudaMemsetAsync(cs.label.get(), 0, ms * sizeof(uint32_t), s));
-    PCR_CUDA(cudaMemsetAsync(cs.ie.get(), 0, ms * sizeof(uint32_t), s));
-    PCR_CUDA(cudaMemsetAsync(cs.edge.get(), 0, ms * sizeof(uint32_t), s));
-    PCR_CUDA(cudaMemsetAsync(cs.kind.get(), 0, ms, s));
-    PCR_CUDA(cudaMemsetAsync(cs.pos.get(), 0, 3 * ms * sizeof(double), s));
-    PCR_CUDA(cudaMemsetAsync(cs.nrm.get(), 0, 3 * ms * sizeof(double), s));
-    uint32_t row = 0;
-    const GridView gv = grid.view();
-    for (uint32_t t = 0; t < n_tx; ++t) {
-      const V3 txp = load3(&scene.h_tx[3ull * t]);
-      if (txs[t].n_los) {
-        count_launch();
-        los_rows_kernel<<<nb(txs[t].n_los), 256, 0, s>>>(txs[t].los_ie.get(), txs[t].n_los, gv, txp, scene.h_tx_id[t], row,
-                                                          cs.rx_id.get(), cs.rx_pos.get(), cs.length.get(),
-                                                          cs.n_inter.get(), cs.tx_id.get(), cs.tx_pos.get());
-        PCR_LAUNCH_CHECK();
-        row += txs[t].n_los;
-      }
-      const CandDev& c = props[t];
-      if (c.n) {
-        PCR_CUDA(cudaMemcpyAsync(cs.rx_id.get() + row, c.rx_id.get(), c.n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-        PCR_CUDA(cudaMemcpyAsync(cs.n_inter.get() + row, c.n_inter.get(), c.n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-        PCR_CUDA(cudaMemcpyAsync(cs.rx_pos.get() + 3ull * row, c.rx_pos.get(), 3ull * c.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        PCR_CUDA(cudaMemcpyAsync(cs.length.get() + row, c.length.get(), c.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        const size_t q = static_cast<size_t>(row) * stride, cnt = static_cast<size_t>(c.n) * stride;
-        PCR_CUDA(cudaMemcpyAsync(cs.label.get() + q, c.label.get(), cnt * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-        PCR_CUDA(cudaMemcpyAsync(cs.ie.get() + q, c.ie.get(), cnt * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-        PCR_CUDA(cudaMemcpyAsync(cs.edge.get() + q, c.edge.get(), cnt * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-        PCR_CUDA(cudaMemcpyAsync(cs.kind.get() + q, c.kind.get(), cnt, cudaMemcpyDeviceToDevice, s));
-        PCR_CUDA(cudaMemcpyAsync(cs.pos.get() + 3 * q, c.pos.get(), 3 * cnt * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        PCR_CUDA(cudaMemcpyAsync(cs.nrm.get() + 3 * q, c.nrm.get(), 3 * cnt * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        count_launch();
-        tx_rows_kernel<<<nb(c.n), 256, 0, s>>>(c.n, row, txp, scene.h_tx_id[t], cs.tx_id.get(), cs.tx_pos.get());
-        PCR_LAUNCH_CHECK();
-        row += c.n;
-      }
-    }
-    PCR_CUDA(cudaStreamSynchronize(s));
-  } catch (const std::exception& e) {
-    fail("trace", e);
-  }
-  S->coarse_paths = cs.n;
-  timing("trace", since(t0));
+  return tp;
+}
 
-  // refine
-  t0 = Clock::now();
-  std::vector<EP> exact;
-  try {
-    pcr_refine_params rp{cfg.delta, cfg.rho, cfg.step_size, cfg.fresnel_enabled};
-    RefineDevIn in{cs.n,         stride,        cs.tx_pos.get(), cs.rx_pos.get(), cs.pos.get(), cs.nrm.get(),
-                   cs.length.get(), cs.n_inter.get(), cs.label.get(), cs.edge.get(), cs.kind.get()};
-    RefineDevOut ro;
-    refine_device(ctx, grid, scene, in, rp, ro);
-    S->refine_trials = ro.trials;
-    S->refine_marches = ro.marches;
-    const size_t n = cs.n, ms = n * stride;
-    std::vector<uint8_t> has(n), kind(ms);
-    std::vector<int32_t> reason(n);
-    std::vector<uint32_t> txid(n), rxid(n), ni(n), lab(ms), ie(ms), ed(ms), iters(n);
-    std::vector<double> txp(3 * n), rxp(3 * n), pos(3 * ms), nrm(3 * ms), len(n), del(n), gn(n);
-    d2h(has.data(), ro.has_path.get(), n, s);
-    d2h(reason.data(), ro.reason.get(), n, s);
-    d2h(iters.data(), ro.iters.get(), n, s);
-    d2h(txid.data(), cs.tx_id.get(), n, s);
-    d2h(rxid.data(), cs.rx_id.get(), n, s);
-    d2h(ni.data(), cs.n_inter.get(), n, s);
-    d2h(kind.data(), cs.kind.get(), ms, s);
-    d2h(ie.data(), cs.ie.get(), ms, s);
-    d2h(ed.data(), cs.edge.get(), ms, s);
-    d2h(txp.data(), cs.tx_pos.get(), 3 * n, s);
-    d2h(rxp.data(), cs.rx_pos.get(), 3 * n, s);
-    d2h(pos.data(), ro.pos.get(), 3 * ms, s);
-    d2h(nrm.data(), ro.nrm.get(), 3 * ms, s);
-    d2h(lab.data(), ro.label.get(), ms, s);
-    d2h(len.data(), ro.length.get(), n, s);
-    d2h(del.data(), ro.delay.get(), n, s);
-    d2h(gn.data(), ro.gnorm.get(), n, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
-    for (size_t i = 0; i < n; ++i) {
-      S->refine_iterations += iters[i];
-      if (!has[i]) {
-        ++S->rejected[reason[i] & 3];
-        continue;
-      }
-      EP e;
-      e.tx_id = txid[i];
-      e.rx_id = rxid[i];
-      e.tx = load3(&txp[3 * i]);
-      e.rx = load3(&rxp[3 * i]);
-      e.total_length = len[i];
-      e.delay = del[i];
-      e.gnorm = gn[i];
-      e.converged = true;
-      for (uint32_t q = 0; q < ni[i]; ++q) {
-        const size_t j = i * stride + q;
-        e.its.push_back(It{kind[j], load3(&pos[3 * j]), load3(&nrm[3 * j]), lab[j], ie[j], ed[j]});
-      }
-      exact.push_back(std::move(e));
+uint32_t stride_of(const pcr_run_config& cfg) { return static_cast<uint32_t>(std::max(1, cfg.max_interactions)); }
+
+// transmission_phase for every TX (full IE range on every shard: it is O(n_IE) and
+// its LOS list heads each TX's candidates).
+void stage_transmission(Ctx& ctx, const GridDev& grid, const SceneDev& scene, std::vector<TxDev>& txs,
+                        pcr_summary* S) {
+  const uint32_t n_tx = static_cast<uint32_t>(scene.h_tx_id.size());
+  txs.resize(n_tx);
+  for (uint32_t t = 0; t < n_tx; ++t) {
+    transmission_device(ctx, grid, scene, t, txs[t]);
+    S->transmission_rays += grid.n_ies;
+    S->visibility_tests += grid.n_ies;
+  }
+}
+
+void release_hits(TxDev& t) {
+  t.hit_ie.release();
+  t.hit_kind.release();
+  t.hit_pos.release();
+  t.hit_nrm.release();
+  t.hit_inc.release();
+}
+
+// One TX's propagated candidates: rows [off, off + n) of a CandDev.
+struct PropSlice {
+  const CandDev* c;
+  uint32_t off, n;
+};
+
+// The candidate list of run_pipeline (pipeline.cpp:136-146): per TX, LOS in IE order,
+// then the propagated candidates in output order.
+void assemble_cands(Ctx& ctx, const SceneDev& scene, const GridDev& grid, const std::vector<TxDev>& txs,
+                    const std::vector<PropSlice>& props, uint32_t stride, CandSet& cs) {
+  cudaStream_t s = ctx.stream;
+  const uint32_t n_tx = static_cast<uint32_t>(txs.size());
+  uint64_t total = 0;
+  for (uint32_t t = 0; t < n_tx; ++t) total += txs[t].n_los + props[t].n;
+  if (total > 0xffffffffull) throw Error(PCR_ERR_NOMEM, "too many candidates");
+  cs.stride = stride;
+  cs.n = static_cast<uint32_t>(total);
+  const size_t m = total ? total : 1, ms = m * stride;
+  cs.tx_id.alloc(m, s);
+  cs.rx_id.alloc(m, s);
+  cs.n_inter.alloc(m, s);
+  cs.label.alloc(ms, s);
+  cs.ie.alloc(ms, s);
+  cs.edge.alloc(ms, s);
+  cs.kind.alloc(ms, s);
+  cs.tx_pos.alloc(3 * m, s);
+  cs.rx_pos.alloc(3 * m, s);
+  cs.length.alloc(m, s);
+  cs.pos.alloc(3 * ms, s);
+  cs.nrm.alloc(3 * ms, s);
+  PCR_CUDA(cudaMemsetAsync(cs.label.get(), 0, ms * sizeof(uint32_t), s));
+  PCR_CUDA(cudaMemsetAsync(cs.ie.get(), 0, ms * sizeof(uint32_t), s));
+  PCR_CUDA(cudaMemsetAsync(cs.edge.get(), 0, ms * sizeof(uint32_t), s));
+  PCR_CUDA(cudaMemsetAsync(cs.kind.get(), 0, ms, s));
+  PCR_CUDA(cudaMemsetAsync(cs.pos.get(), 0, 3 * ms * sizeof(double), s));
+  PCR_CUDA(cudaMemsetAsync(cs.nrm.get(), 0, 3 * ms * sizeof(double), s));
+  uint32_t row = 0;
+  const GridView gv = grid.view();
+  for (uint32_t t = 0; t < n_tx; ++t) {
+    const V3 txp = load3(&scene.h_tx[3ull * t]);
+    if (txs[t].n_los) {
+      count_launch();
+      los_rows_kernel<<<nb(txs[t].n_los), 256, 0, s>>>(txs[t].los_ie.get(), txs[t].n_los, gv, txp, scene.h_tx_id[t], row,
+                                                        cs.rx_id.get(), cs.rx_pos.get(), cs.length.get(),
+                                                        cs.n_inter.get(), cs.tx_id.get(), cs.tx_pos.get());
+      PCR_LAUNCH_CHECK();
+      row += txs[t].n_los;
     }
-  } catch (const std::exception& e) {
-    fail("refine", e);
+    const PropSlice& p = props[t];
+    if (p.n) {
+      const CandDev& c = *p.c;
+      const size_t o = p.off, n = p.n;
+      auto cp = [&](auto* dst, const auto* src, size_t count) {
+        PCR_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(*src), cudaMemcpyDeviceToDevice, s));
+      };
+      cp(cs.rx_id.get() + row, c.rx_id.get() + o, n);
+      cp(cs.n_inter.get() + row, c.n_inter.get() + o, n);
+      cp(cs.rx_pos.get() + 3ull * row, c.rx_pos.get() + 3 * o, 3 * n);
+      cp(cs.length.get() + row, c.length.get() + o, n);
+      const size_t q = static_cast<size_t>(row) * stride, qo = o * c.stride, cnt = n * stride;
+      if (c.stride != stride) throw Error(PCR_ERR_RUNTIME, "trace: candidate stride mismatch");
+      cp(cs.label.get() + q, c.label.get() + qo, cnt);
+      cp(cs.ie.get() + q, c.ie.get() + qo, cnt);
+      cp(cs.edge.get() + q, c.edge.get() + qo, cnt);
+      cp(cs.kind.get() + q, c.kind.get() + qo, cnt);
+      cp(cs.pos.get() + 3 * q, c.pos.get() + 3 * qo, 3 * cnt);
+      cp(cs.nrm.get() + 3 * q, c.nrm.get() + 3 * qo, 3 * cnt);
+      count_launch();
+      tx_rows_kernel<<<nb(p.n), 256, 0, s>>>(p.n, row, txp, scene.h_tx_id[t], cs.tx_id.get(), cs.tx_pos.get());
+      PCR_LAUNCH_CHECK();
+      row += p.n;
+    }
+  }
+  PCR_CUDA(cudaStreamSynchronize(s));
+}
+
+void refine_cands(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const CandSet& cs, const pcr_run_config& cfg,
+                  uint32_t first, uint32_t step, RefineDevOut& ro) {
+  pcr_refine_params rp{cfg.delta, cfg.rho, cfg.step_size, cfg.fresnel_enabled};
+  RefineDevIn in{cs.n,         cs.stride,       cs.tx_pos.get(), cs.rx_pos.get(), cs.pos.get(), cs.nrm.get(),
+                 cs.length.get(), cs.n_inter.get(), cs.label.get(), cs.edge.get(), cs.kind.get()};
+  in.first = first;
+  in.step = step;
+  refine_device(ctx, grid, scene, in, rp, ro);
+}
+
+// Refinement outcomes -> ExactPaths (pipeline.cpp:148-187), counting rejects and
+// iterations; LOS candidates pass through.
+std::vector<EP> collect_paths(Ctx& ctx, const CandSet& cs, const RefineDevOut& ro, pcr_summary* S) {
+  cudaStream_t s = ctx.stream;
+  const uint32_t stride = cs.stride;
+  const size_t n = cs.n, ms = n * stride;
+  std::vector<uint8_t> has(n), kind(ms);
+  std::vector<int32_t> reason(n);
+  std::vector<uint32_t> txid(n), rxid(n), ni(n), lab(ms), ie(ms), ed(ms), iters(n);
+  std::vector<double> txp(3 * n), rxp(3 * n), pos(3 * ms), nrm(3 * ms), len(n), del(n), gn(n);
+  d2h(has.data(), ro.has_path.get(), n, s);
+  d2h(reason.data(), ro.reason.get(), n, s);
+  d2h(iters.data(), ro.iters.get(), n, s);
+  d2h(txid.data(), cs.tx_id.get(), n, s);
+  d2h(rxid.data(), cs.rx_id.get(), n, s);
+  d2h(ni.data(), cs.n_inter.get(), n, s);
+  d2h(kind.data(), cs.kind.get(), ms, s);
+  d2h(ie.data(), cs.ie.get(), ms, s);
+  d2h(ed.data(), cs.edge.get(), ms, s);
+  d2h(txp.data(), cs.tx_pos.get(), 3 * n, s);
+  d2h(rxp.data(), cs.rx_pos.get(), 3 * n, s);
+  d2h(pos.data(), ro.pos.get(), 3 * ms, s);
+  d2h(nrm.data(), ro.nrm.get(), 3 * ms, s);
+  d2h(lab.data(), ro.label.get(), ms, s);
+  d2h(len.data(), ro.length.get(), n, s);
+  d2h(del.data(), ro.delay.get(), n, s);
+  d2h(gn.data(), ro.gnorm.get(), n, s);
+  PCR_CUDA(cudaStreamSynchronize(s));
+  std::vector<EP> exact;
+  for (size_t i = 0; i < n; ++i) {
+    S->refine_iterations += iters[i];
+    if (!has[i]) {
+      ++S->rejected[reason[i] & 3];
+      continue;
+    }
+    EP e;
+    e.tx_id = txid[i];
+    e.rx_id = rxid[i];
+    e.tx = load3(&txp[3 * i]);
+    e.rx = load3(&rxp[3 * i]);
+    e.total_length = len[i];
+    e.delay = del[i];
+    e.gnorm = gn[i];
+    e.converged = true;
+    for (uint32_t q = 0; q < ni[i]; ++q) {
+      const size_t j = i * stride + q;
+      e.its.push_back(It{kind[j], load3(&pos[3 * j]), load3(&nrm[3 * j]), lab[j], ie[j], ed[j]});
+    }
+    exact.push_back(std::move(e));
   }
   S->refined_paths = exact.size();
-  timing("refine", since(t0));
+  return exact;
+}
 
-  t0 = Clock::now();
+// dedup_by_label, dedup_by_fresnel, final order (pipeline.cpp:189-207) -> S->paths
+void finish_paths(std::vector<EP> exact, const pcr_run_config& cfg, pcr_summary* S) {
   exact = dedup_by_label(std::move(exact));
   if (cfg.fresnel_enabled) exact = dedup_by_fresnel(std::move(exact), cfg.carrier_frequency_hz);
   final_sort(exact);
@@ -585,8 +613,359 @@ void run_pipeline_core(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cf
   put_paths(P, exact);
   S->paths = *P;
   std::free(P);
-  timing("dedup", since(t0));
-  *out = S;
+}
+
+}  // namespace
+
+void run_pipeline_core(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, pcr_summary** out,
+                       double upload_seconds) {
+  Run run(cfg, scene);
+  pcr_summary* S = run.S;
+  const uint32_t n_tx = static_cast<uint32_t>(scene.h_tx_id.size());
+
+  auto t0 = Clock::now();
+  stage_validate(ctx, scene);
+  run.timing("validate", since(t0) + upload_seconds);
+
+  t0 = Clock::now();
+  GridDev grid;
+  stage_voxelize(ctx, scene, cfg, grid, S);
+  run.timing("voxelize", since(t0));
+
+  // trace
+  t0 = Clock::now();
+  const pcr_trace_params tp = trace_params_of(cfg);
+  CandSet cs;
+  try {
+    std::vector<TxDev> txs;
+    std::vector<CandDev> props(n_tx);
+    std::vector<PropSlice> slices(n_tx);
+    stage_transmission(ctx, grid, scene, txs, S);
+    TraceStats st;
+    for (uint32_t t = 0; t < n_tx; ++t) {
+      propagate_device(ctx, grid, scene, t, txs[t].hit_ie.get(), txs[t].hit_kind.get(), txs[t].hit_pos.get(),
+                       txs[t].hit_nrm.get(), txs[t].hit_inc.get(), txs[t].n_hits, tp, props[t], st);
+      release_hits(txs[t]);
+      slices[t] = PropSlice{&props[t], 0, props[t].n};
+    }
+    S->cone_traces = st.cone_traces;
+    S->walk_cells = st.walk_cells;
+    S->walk_ies = st.walk_ies;
+    S->visibility_tests += st.visibility_tests;
+    assemble_cands(ctx, scene, grid, txs, slices, stride_of(cfg), cs);
+  } catch (const std::exception& e) {
+    stage_fail("trace", e);
+  }
+  S->coarse_paths = cs.n;
+  run.timing("trace", since(t0));
+
+  // refine
+  t0 = Clock::now();
+  std::vector<EP> exact;
+  try {
+    RefineDevOut ro;
+    refine_cands(ctx, grid, scene, cs, cfg, 0, 1, ro);
+    S->refine_trials = ro.trials;
+    S->refine_marches = ro.marches;
+    exact = collect_paths(ctx, cs, ro, S);
+  } catch (const std::exception& e) {
+    stage_fail("refine", e);
+  }
+  run.timing("refine", since(t0));
+
+  t0 = Clock::now();
+  finish_paths(std::move(exact), cfg, S);
+  run.timing("dedup", since(t0));
+  *out = run.release();
+}
+
+// ---- sharded pipeline ---------------------------------------------------------
+// A shard traces the initial hits t ≡ shard (mod n_shards) of every TX and keeps its
+// own first-kappa (exact pre-cap); the rows of every shard are merged by DFS key into
+// the global candidate list (identical on every shard); a shard refines candidates
+// i ≡ shard (mod n_shards); one shard collects every outcome row and finishes.
+struct ShardState {
+  pcr_run_config cfg{};
+  uint32_t shard = 0, n_shards = 1;
+  GridDev grid;
+  std::vector<TxDev> txs;
+  pcr_summary head{};  // counts and timings of this shard so far
+  double trace_s = 0, refine_s = 0;
+  pcr_shard_stats stats{};
+  DBuf<uint8_t> rows;
+  uint64_t n_rows = 0;
+  CandSet cs;
+  bool merged = false;
+  DBuf<uint8_t> out_rows;
+  uint64_t n_out = 0;
+};
+
+namespace {
+
+ShardState& shard_state(Ctx& ctx) {
+  if (!ctx.shard) throw Error(PCR_ERR_INVALID, "shard: pcr_shard_trace has not run on this context");
+  return *ctx.shard;
+}
+
+void head_timing(pcr_summary& S, const char* name, double sec) {
+  if (S.n_timings < PCR_MAX_STAGES) {
+    std::snprintf(S.timing_stage[S.n_timings], 16, "%s", name);
+    S.timing_seconds[S.n_timings++] = sec;
+  }
+}
+
+__global__ void pack_outcomes_kernel(uint32_t n_sub, uint32_t first, uint32_t step, uint32_t stride,
+                                     const int32_t* __restrict__ reason, const uint8_t* __restrict__ has,
+                                     const uint32_t* __restrict__ iters, const double* __restrict__ length,
+                                     const double* __restrict__ delay, const double* __restrict__ gnorm,
+                                     const double* __restrict__ pos, const double* __restrict__ nrm,
+                                     const uint32_t* __restrict__ label, uint8_t* __restrict__ rows) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_sub) return;
+  const uint32_t k = first + i * step;
+  uint8_t* r = rows + static_cast<size_t>(i) * out_row_bytes(stride);
+  OutRowHead h{k, reason[k], iters[k], has[k], length[k], delay[k], gnorm[k]};
+  *reinterpret_cast<OutRowHead*>(r) = h;
+  OutRowLevel* lv = reinterpret_cast<OutRowLevel*>(r + sizeof(OutRowHead));
+  for (uint32_t q = 0; q < stride; ++q) {
+    const size_t j = static_cast<size_t>(k) * stride + q;
+    OutRowLevel l;
+    for (int a = 0; a < 3; ++a) {
+      l.pos[a] = pos[3 * j + a];
+      l.nrm[a] = nrm[3 * j + a];
+    }
+    l.label = label[j];
+    l.pad = 0;
+    lv[q] = l;
+  }
+}
+
+__global__ void unpack_outcomes_kernel(const uint8_t* __restrict__ rows, uint64_t n_rows, uint32_t n, uint32_t stride,
+                                       int32_t* reason, uint8_t* has, uint32_t* iters, double* length, double* delay,
+                                       double* gnorm, double* pos, double* nrm, uint32_t* label, uint32_t* seen,
+                                       int* bad) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_rows) return;
+  const uint8_t* r = rows + i * out_row_bytes(stride);
+  const OutRowHead& h = *reinterpret_cast<const OutRowHead*>(r);
+  const uint32_t k = h.cand;
+  if (k >= n || atomicAdd(seen + k, 1u) != 0) {
+    *bad = 1;
+    return;
+  }
+  reason[k] = h.reason;
+  has[k] = static_cast<uint8_t>(h.has_path);
+  iters[k] = h.iters;
+  length[k] = h.length;
+  delay[k] = h.delay;
+  gnorm[k] = h.gnorm;
+  const OutRowLevel* lv = reinterpret_cast<const OutRowLevel*>(r + sizeof(OutRowHead));
+  for (uint32_t q = 0; q < stride; ++q) {
+    const size_t j = static_cast<size_t>(k) * stride + q;
+    for (int a = 0; a < 3; ++a) {
+      pos[3 * j + a] = lv[q].pos[a];
+      nrm[3 * j + a] = lv[q].nrm[a];
+    }
+    label[j] = lv[q].label;
+  }
+}
+
+}  // namespace
+
+void api_shard_trace(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, uint32_t shard, uint32_t n_shards,
+                     uint64_t* n_rows, uint64_t* row_bytes) {
+  if (n_shards == 0 || shard >= n_shards) throw Error(PCR_ERR_INVALID, "shard: index out of range");
+  ctx.shard = std::make_shared<ShardState>();
+  ShardState& st = *ctx.shard;
+  st.cfg = cfg;
+  st.shard = shard;
+  st.n_shards = n_shards;
+  pcr_summary& S = st.head;
+  S.hash = config_hash(cfg);
+  S.point_count = scene.n_points;
+  S.edge_count = scene.n_edges;
+  const uint32_t n_tx = static_cast<uint32_t>(scene.h_tx_id.size());
+  const uint32_t stride = stride_of(cfg);
+
+  auto t0 = Clock::now();
+  stage_validate(ctx, scene);
+  head_timing(S, "validate", since(t0));
+  t0 = Clock::now();
+  stage_voxelize(ctx, scene, cfg, st.grid, &S);
+  head_timing(S, "voxelize", since(t0));
+
+  t0 = Clock::now();
+  try {
+    cudaStream_t s = ctx.stream;
+    const pcr_trace_params tp = trace_params_of(cfg);
+    stage_transmission(ctx, st.grid, scene, st.txs, &S);
+    std::vector<CandDev> props(n_tx);
+    TraceStats ts;
+    uint64_t total = 0;
+    for (uint32_t t = 0; t < n_tx; ++t) {
+      TxDev& x = st.txs[t];
+      propagate_device(ctx, st.grid, scene, t, x.hit_ie.get(), x.hit_kind.get(), x.hit_pos.get(), x.hit_nrm.get(),
+                       x.hit_inc.get(), x.n_hits, tp, props[t], ts, shard, n_shards, true);
+      release_hits(x);
+      total += props[t].n;
+    }
+    st.stats.cone_traces = ts.cone_traces;
+    st.stats.visibility_tests = ts.visibility_tests;
+    st.stats.walk_cells = ts.walk_cells;
+    st.stats.walk_ies = ts.walk_ies;
+    const size_t bytes = cand_row_bytes(stride);
+    st.rows.alloc(total ? total * bytes : 1, s);
+    uint64_t row = 0;
+    for (uint32_t t = 0; t < n_tx; ++t) {
+      pack_cand_rows(ctx, props[t], t, st.rows.get() + row * bytes);
+      row += props[t].n;
+    }
+    st.n_rows = total;
+    PCR_CUDA(cudaStreamSynchronize(s));
+  } catch (const std::exception& e) {
+    stage_fail("trace", e);
+  }
+  st.trace_s = since(t0);
+  *n_rows = st.n_rows;
+  *row_bytes = cand_row_bytes(stride);
+}
+
+void api_shard_rows(Ctx& ctx, void* dst) {
+  ShardState& st = shard_state(ctx);
+  if (st.n_rows)
+    PCR_CUDA(cudaMemcpyAsync(dst, st.rows.get(), st.n_rows * cand_row_bytes(stride_of(st.cfg)),
+                             cudaMemcpyDeviceToDevice, ctx.stream));
+  PCR_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+void api_shard_refine(Ctx& ctx, const SceneDev& scene, const void* rows, uint64_t n_rows, uint64_t* n_out,
+                      uint64_t* out_bytes) {
+  ShardState& st = shard_state(ctx);
+  cudaStream_t s = ctx.stream;
+  const uint32_t stride = stride_of(st.cfg);
+  const uint32_t n_tx = static_cast<uint32_t>(scene.h_tx_id.size());
+  auto t0 = Clock::now();
+  try {
+    CandDev merged;
+    std::vector<uint32_t> per_tx;
+    kappa_merge_rows(ctx, static_cast<const uint8_t*>(rows), n_rows, stride, st.cfg.kappa, n_tx, merged, per_tx);
+    std::vector<PropSlice> slices(n_tx);
+    uint32_t off = 0;
+    for (uint32_t t = 0; t < n_tx; ++t) {
+      slices[t] = PropSlice{&merged, off, per_tx[t]};
+      off += per_tx[t];
+    }
+    assemble_cands(ctx, scene, st.grid, st.txs, slices, stride, st.cs);
+    st.merged = true;
+  } catch (const std::exception& e) {
+    stage_fail("trace", e);
+  }
+  st.trace_s += since(t0);
+  st.head.coarse_paths = st.cs.n;
+
+  t0 = Clock::now();
+  try {
+    RefineDevOut ro;
+    refine_cands(ctx, st.grid, scene, st.cs, st.cfg, st.shard, st.n_shards, ro);
+    st.stats.refine_trials = ro.trials;
+    st.stats.refine_marches = ro.marches;
+    const uint32_t n = st.cs.n;
+    const uint32_t n_sub = n > st.shard ? (n - st.shard + st.n_shards - 1) / st.n_shards : 0;
+    const size_t bytes = out_row_bytes(stride);
+    st.out_rows.alloc(n_sub ? n_sub * bytes : 1, s);
+    st.n_out = n_sub;
+    if (n_sub) {
+      count_launch();
+      pack_outcomes_kernel<<<nb(n_sub), 256, 0, s>>>(n_sub, st.shard, st.n_shards, stride, ro.reason.get(),
+                                                      ro.has_path.get(), ro.iters.get(), ro.length.get(),
+                                                      ro.delay.get(), ro.gnorm.get(), ro.pos.get(), ro.nrm.get(),
+                                                      ro.label.get(), st.out_rows.get());
+      PCR_LAUNCH_CHECK();
+      // iterations of this shard's candidates (a work counter, summed over shards)
+      std::vector<uint32_t> all(n);
+      d2h(all.data(), ro.iters.get(), n, s);
+      PCR_CUDA(cudaStreamSynchronize(s));
+      uint64_t sum = 0;
+      for (uint32_t i = 0; i < n_sub; ++i) sum += all[st.shard + static_cast<size_t>(i) * st.n_shards];
+      st.stats.refine_iterations = sum;
+    }
+    PCR_CUDA(cudaStreamSynchronize(s));
+  } catch (const std::exception& e) {
+    stage_fail("refine", e);
+  }
+  st.refine_s = since(t0);
+  *n_out = st.n_out;
+  *out_bytes = out_row_bytes(stride);
+}
+
+void api_shard_outcomes(Ctx& ctx, void* dst) {
+  ShardState& st = shard_state(ctx);
+  if (st.n_out)
+    PCR_CUDA(cudaMemcpyAsync(dst, st.out_rows.get(), st.n_out * out_row_bytes(stride_of(st.cfg)),
+                             cudaMemcpyDeviceToDevice, ctx.stream));
+  PCR_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+void api_shard_stats(Ctx& ctx, pcr_shard_stats* out) { *out = shard_state(ctx).stats; }
+
+void api_shard_finish(Ctx& ctx, const void* rows, uint64_t n_rows, const pcr_shard_stats& totals,
+                      pcr_summary** out) {
+  ShardState& st = shard_state(ctx);
+  if (!st.merged) throw Error(PCR_ERR_INVALID, "shard: pcr_shard_refine has not run on this context");
+  cudaStream_t s = ctx.stream;
+  const CandSet& cs = st.cs;
+  const uint32_t stride = cs.stride;
+  auto t0 = Clock::now();
+  Run run(halloc<pcr_summary>(1));
+  pcr_summary* S = run.S;
+  *S = st.head;  // hash, sizes, transmission counts, validate + voxelize timings
+  S->cone_traces = totals.cone_traces;
+  S->walk_cells = totals.walk_cells;
+  S->walk_ies = totals.walk_ies;
+  S->visibility_tests += totals.visibility_tests;
+  S->refine_trials = totals.refine_trials;
+  S->refine_marches = totals.refine_marches;
+  run.timing("trace", st.trace_s);
+  std::vector<EP> exact;
+  try {
+    if (n_rows != cs.n) throw Error(PCR_ERR_INVALID, "shard: outcome rows do not cover the candidate list");
+    RefineDevOut ro;
+    const size_t m = cs.n ? cs.n : 1, ms = m * stride;
+    ro.reason.alloc(m, s);
+    ro.has_path.alloc(m, s);
+    ro.iters.alloc(m, s);
+    ro.length.alloc(m, s);
+    ro.delay.alloc(m, s);
+    ro.gnorm.alloc(m, s);
+    ro.pos.alloc(3 * ms, s);
+    ro.nrm.alloc(3 * ms, s);
+    ro.label.alloc(ms, s);
+    DBuf<uint32_t> seen(m, s);
+    DBuf<int> bad(1, s);
+    PCR_CUDA(cudaMemsetAsync(seen.get(), 0, m * sizeof(uint32_t), s));
+    PCR_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+    if (n_rows) {
+      count_launch();
+      unpack_outcomes_kernel<<<nb(n_rows), 256, 0, s>>>(static_cast<const uint8_t*>(rows), n_rows, cs.n, stride,
+                                                         ro.reason.get(), ro.has_path.get(), ro.iters.get(),
+                                                         ro.length.get(), ro.delay.get(), ro.gnorm.get(),
+                                                         ro.pos.get(), ro.nrm.get(), ro.label.get(), seen.get(),
+                                                         bad.get());
+      PCR_LAUNCH_CHECK();
+    }
+    int h_bad = 0;
+    d2h(&h_bad, bad.get(), 1, s);
+    PCR_CUDA(cudaStreamSynchronize(s));
+    if (h_bad) throw Error(PCR_ERR_INVALID, "shard: outcome rows do not cover the candidate list");
+    exact = collect_paths(ctx, cs, ro, S);
+  } catch (const std::exception& e) {
+    stage_fail("refine", e);
+  }
+  run.timing("refine", st.refine_s + since(t0));
+  t0 = Clock::now();
+  finish_paths(std::move(exact), st.cfg, S);
+  run.timing("dedup", since(t0));
+  *out = run.release();
 }
 
 }  // namespace pcr

@@ -21,6 +21,16 @@ void api_refine_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, cons
 // pipeline (pipeline.cu)
 void api_run_pipeline_on_scene(Ctx& ctx, const pcr_scene_desc& desc, const pcr_run_config& cfg, pcr_summary** out);
 void api_run_pipeline_device(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, pcr_summary** out);
+// sharded pipeline (pipeline.cu)
+void api_shard_trace(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, uint32_t shard, uint32_t n_shards,
+                     uint64_t* n_rows, uint64_t* row_bytes);
+void api_shard_rows(Ctx& ctx, void* dst);
+void api_shard_refine(Ctx& ctx, const SceneDev& scene, const void* rows, uint64_t n_rows, uint64_t* n_out,
+                      uint64_t* out_bytes);
+void api_shard_outcomes(Ctx& ctx, void* dst);
+void api_shard_stats(Ctx& ctx, pcr_shard_stats* out);
+void api_shard_finish(Ctx& ctx, const void* rows, uint64_t n_rows, const pcr_shard_stats& totals,
+                      pcr_summary** out);
 void upload_scene(Ctx& ctx, const pcr_scene_desc& d, SceneDev& S);
 uint64_t config_hash(const pcr_run_config& c);
 void run_config_defaults(pcr_run_config* c);

@@ -86,30 +86,57 @@ __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, c
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   for (int pass = 0; pass < 2; ++pass) {
     const bool same = pass == 0;
-    bool found = false;
-    uint32_t best_ie = 0;
+    uint32_t best_ie = kNoIe;
     double best_t = 1.7976931348623157e308;
-    Reproj best;
-    for (int z = lo[2]; z <= hi[2]; ++z)
-      for (int y = lo[1]; y <= hi[1]; ++y)
-        for (int x = lo[0]; x <= hi[0]; ++x) {
-          const int4 cell = g.cells[linear_index(g, x, y, z)];
-          for (uint32_t i = static_cast<uint32_t>(cell.x); i < static_cast<uint32_t>(cell.y); ++i) {
-            if ((g.ie_meta[i] & 3u) != kSurface) continue;
-            const double4 sc4 = g.ie_sc[i];
-            if (!(norm(ld3(sc4) - predicted) <= radius + sc4.w)) continue;
-            if (same != (g.ie_label[i] == label)) continue;
-            SurfaceHit hit;
-            ++n_march;
-            if (!march_segment(prev, dir, i, g, s, inf, &hit)) continue;
-            if (hit.distance >= best_t) continue;
-            best_t = hit.distance;
-            best = Reproj{hit.position, hit.normal, g.ie_label[i]};
-            best_ie = i;
-            found = true;
+    Reproj best;  // only for a non-planar winner; planar winners are rebuilt below
+    // one flat loop over (cell z→y→x, IE in cell order): lanes of a warp stay in the
+    // same loop body whatever their cells' occupancy
+    int x = lo[0], y = lo[1], z = lo[2];
+    int4 cell = g.cells[linear_index(g, x, y, z)];
+    uint32_t i = static_cast<uint32_t>(cell.x);
+    for (;;) {
+      if (i >= static_cast<uint32_t>(cell.y)) {
+        if (++x > hi[0]) {
+          x = lo[0];
+          if (++y > hi[1]) {
+            y = lo[1];
+            if (++z > hi[2]) break;
           }
         }
-    if (found) {
+        cell = g.cells[linear_index(g, x, y, z)];
+        i = static_cast<uint32_t>(cell.x);
+        continue;
+      }
+      const uint32_t ie = i++;
+      // the three filters are pure predicates: cheapest first
+      if (same != (g.ie_label[ie] == label)) continue;
+      if ((g.ie_meta[ie] & 3u) != kSurface) continue;
+      const double4 sc4 = g.ie_sc[ie];
+      if (!norm_le(ld3(sc4) - predicted, radius + sc4.w)) continue;
+      ++n_march;  // counts the reference's march_segment call
+      // march_segment's window (surface.cpp:64-72): every hit it returns lies at
+      // t >= t_lo, so a window starting at or past the best t cannot win (strict <)
+      const double t_center = dot(ld3(sc4) - prev, dir);
+      const double t_lo = smax(0.0, t_center - sc4.w);
+      if (t_lo >= best_t) continue;
+      if (ie_planar(g, ie)) {
+        double t;
+        if (!planar_march_t(prev, dir, ie, g, t_lo, t_center + sc4.w, t)) continue;
+        if (t >= best_t) continue;
+        best_t = t;
+        best_ie = ie;
+      } else {
+        SurfaceHit hit;
+        if (!march_segment(prev, dir, ie, g, s, inf, &hit)) continue;
+        if (hit.distance >= best_t) continue;
+        best_t = hit.distance;
+        best = Reproj{hit.position, hit.normal, g.ie_label[ie]};
+        best_ie = ie;
+      }
+    }
+    if (best_ie != kNoIe) {
+      if (ie_planar(g, best_ie))  // make_hit's record (surface.cpp:98-106)
+        best = Reproj{prev + best_t * dir, ld3(g.ie_pn[best_ie]), g.ie_label[best_ie]};
       polish(best, best_ie, g, s);
       out = best;
       return true;
@@ -152,6 +179,7 @@ __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, c
 }
 
 struct CandIn {
+  uint32_t first, step;  // candidate subset first + i * step
   uint32_t stride;
   const double* tx;
   const double* rx;
@@ -231,9 +259,10 @@ __global__ void __launch_bounds__(kRefineThreads, 4) refine_kernel(CandIn in, ui
                                                                    double delta, int rho, double step_size, RefOut o,
                                                                    uint32_t* next_cand) {
   for (;;) {
-    const uint32_t k = atomicAdd(next_cand, 1u);
-    if (k >= n) break;
-    refine_one(k, in, g, s, delta, rho, step_size, o);
+    const uint32_t idx = atomicAdd(next_cand, 1u);
+    if (idx >= n) break;
+    // this shard's candidates are first, first + step, ... (SURVEY 8e round-robin)
+    refine_one(in.first + idx * in.step, in, g, s, delta, rho, step_size, o);
   }
 }
 
@@ -442,7 +471,10 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
   PCR_CUDA(cudaMemcpyAsync(out.nrm.get(), in.nrm, 3 * ms * sizeof(double), cudaMemcpyDeviceToDevice, s));
   PCR_CUDA(cudaMemcpyAsync(out.label.get(), in.label, ms * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
   if (!in.n) return;
-  CandIn ci{in.stride, in.tx, in.rx, in.n_inter, in.kind, in.pos, in.label, in.nrm, in.edge, in.coarse_length};
+  const uint32_t step = in.step ? in.step : 1;
+  const uint32_t n_sub = in.n > in.first ? (in.n - in.first + step - 1) / step : 0;
+  if (!n_sub) return;
+  CandIn ci{in.first, step, in.stride, in.tx, in.rx, in.n_inter, in.kind, in.pos, in.label, in.nrm, in.edge, in.coarse_length};
   DBuf<unsigned long long> stats(2, s);
   DBuf<uint32_t> next(1, s);
   PCR_CUDA(cudaMemsetAsync(next.get(), 0, sizeof(uint32_t), s));
@@ -455,10 +487,10 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     // enough resident threads to fill every SM at the kernel's occupancy
     int per_sm = 0;
     PCR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, kRefineThreads, 0));
-    const uint64_t want = (static_cast<uint64_t>(in.n) + kRefineThreads - 1) / kRefineThreads;
+    const uint64_t want = (static_cast<uint64_t>(n_sub) + kRefineThreads - 1) / kRefineThreads;
     const uint64_t cap = static_cast<uint64_t>(ctx.sm_count) * (per_sm > 0 ? per_sm : 1);
     refine_kernel<<<static_cast<unsigned>(want < cap ? want : cap), kRefineThreads, 0, s>>>(
-        ci, in.n, grid.view(), scene.view(), p.delta, p.rho, p.step_size, ro, next.get());
+        ci, n_sub, grid.view(), scene.view(), p.delta, p.rho, p.step_size, ro, next.get());
   }
   PCR_LAUNCH_CHECK();
   unsigned long long hs[2];

@@ -24,6 +24,7 @@
 
 #include "host_alloc.hpp"
 #include "pipeline.hpp"
+#include "shard_rows.cuh"
 #include "sort.cuh"
 #include "stages.cuh"
 #include "trace.cuh"
@@ -321,17 +322,19 @@ __device__ void transmission_hit(uint32_t i, const V3& tx, const GridView& g, co
 // Root nodes from initial hits (propagate :482-509).
 __global__ void seed_kernel(const uint32_t* __restrict__ ie_index, const uint8_t* __restrict__ kind,
                             const double* __restrict__ pos, const double* __restrict__ nrm,
-                            const double* __restrict__ inc, uint32_t n, GridView g, SceneView s, TraceCfg c,
-                            Node* __restrict__ nodes) {
-  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
+                            const double* __restrict__ inc, uint32_t n, uint32_t task_first, uint32_t task_step,
+                            GridView g, SceneView s, TraceCfg c, Node* __restrict__ nodes) {
+  const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= n) return;
+  // this shard's tasks are initial hits task_first, task_first + task_step, ...
+  const uint32_t k = task_first + slot * task_step;
   const uint32_t i = ie_index[k];
   Node nd;
   nd.parent = kNoNode;
   nd.parent_j = 0;
   nd.ie = i;
   nd.label = g.ie_label[i];
-  nd.task = k;
+  nd.task = k;  // the global task index: DFS keys are shard-independent
   nd.depth = 1;
   nd.pad = 0;
   nd.n_children = 0;
@@ -360,7 +363,7 @@ __global__ void seed_kernel(const uint32_t* __restrict__ ie_index, const uint8_t
     nd.edge = 0;
     store3(nd.nrm, V3{0, 0, 1});
   }
-  nodes[k] = nd;
+  nodes[slot] = nd;
 }
 
 __global__ void children_kernel(const Node* __restrict__ nodes, uint32_t begin, uint32_t n, uint64_t* __restrict__ cnt) {
@@ -478,6 +481,18 @@ __global__ void compact_cands_kernel(const Cand* __restrict__ in, const uint32_t
                                      Cand* __restrict__ out) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n && flag[k]) out[pos[k]] = in[perm[k]];
+}
+
+// keys (word-major, 4 words) and group hashes of the kept candidates, in kept order
+__global__ void compact_keys_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ hash,
+                                    const uint32_t* __restrict__ perm, const uint32_t* __restrict__ flag,
+                                    const uint32_t* __restrict__ pos, uint32_t n, uint32_t n_out,
+                                    uint64_t* __restrict__ keys_out, uint64_t* __restrict__ hash_out) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n || !flag[k]) return;
+  const uint32_t src = perm[k], dst = pos[k];
+  for (int q = 0; q < 4; ++q) keys_out[static_cast<size_t>(q) * n_out + dst] = keys[static_cast<size_t>(q) * n + src];
+  hash_out[dst] = hash[src];
 }
 
 // segmented running max of run starts (heads carry their own index)
@@ -770,7 +785,8 @@ __global__ void count_alive_kernel(const Ray* __restrict__ rays, uint32_t n, uns
 
 // First-kappa selection in DFS order; returns kept candidates (key order) in `out`.
 static void kappa_select(Ctx& ctx, const GridDev& grid, const DBuf<Cand>& cands, uint32_t n, const Node* nodes,
-                         const KeyLayout& L, int kappa, DBuf<Cand>& out, uint32_t& n_out) {
+                         const KeyLayout& L, int kappa, DBuf<Cand>& out, uint32_t& n_out,
+                         DBuf<uint64_t>* keys_out = nullptr, DBuf<uint64_t>* hash_out = nullptr) {
   cudaStream_t s = ctx.stream;
   if (n == 0) {
     n_out = 0;
@@ -833,18 +849,30 @@ static void kappa_select(Ctx& ctx, const GridDev& grid, const DBuf<Cand>& cands,
   count_launch();
   compact_cands_kernel<<<nb(n), kT, 0, s>>>(cands.get(), perm_key.get(), flag.get(), pos.get(), n, o.get());
   PCR_LAUNCH_CHECK();
+  if (keys_out && hash_out) {
+    keys_out->alloc(4ull * (n_out ? n_out : 1), s);
+    hash_out->alloc(n_out ? n_out : 1, s);
+    count_launch();
+    compact_keys_kernel<<<nb(n), kT, 0, s>>>(keys.get(), hash.get(), perm_key.get(), flag.get(), pos.get(), n, n_out,
+                                             keys_out->get(), hash_out->get());
+    PCR_LAUNCH_CHECK();
+  }
   out = std::move(o);
 }
 
 // propagate for one TX from device initial hits; kept candidates materialised.
 void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint32_t tx_index, const uint32_t* hit_ie,
                       const uint8_t* hit_kind, const double* hit_pos, const double* hit_nrm, const double* hit_inc,
-                      uint32_t n_hits, const pcr_trace_params& p, CandDev& out, TraceStats& stats) {
+                      uint32_t n_hits, const pcr_trace_params& p, CandDev& out, TraceStats& stats,
+                      uint32_t shard, uint32_t n_shards, bool want_keys) {
   cudaStream_t s = ctx.stream;
   const TraceCfg c = make_cfg(p);
   out.n = 0;
   out.stride = static_cast<uint32_t>(std::max(1, p.max_interactions));
-  if (p.max_interactions < 1 || n_hits == 0) return;
+  if (n_shards == 0 || shard >= n_shards) throw Error(1, "trace: shard index out of range");
+  // this shard's tasks: initial hits shard, shard + n_shards, ... (SURVEY 8e cyclic split)
+  const uint32_t n_local = n_hits > shard ? (n_hits - shard + n_shards - 1) / n_shards : 0;
+  if (p.max_interactions < 1 || n_local == 0) return;
   if (p.max_interactions > kMaxDepth) throw Error(1, "trace: max_interactions above the supported 8");
   if (p.max_diffractions >= 1 || true) ensure_fan_table(ctx, std::max(1, c.fan_n));
   const FanTable fan{ctx.fan_table.get(), c.fan_n};
@@ -860,12 +888,13 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
   if (L.total > 256) throw Error(1, "trace: DFS key wider than 256 bits");
 
   // node arena
-  size_t node_cap = std::max<size_t>(1u << 20, 2ull * n_hits);
+  size_t node_cap = std::max<size_t>(1u << 20, 2ull * n_local);
   DBuf<Node> nodes(node_cap, s);
   DBuf<uint32_t> counters(2, s);  // n_nodes, n_cands
-  uint32_t n_nodes = n_hits;
+  uint32_t n_nodes = n_local;
   count_launch();
-  seed_kernel<<<nb(n_hits), kT, 0, s>>>(hit_ie, hit_kind, hit_pos, hit_nrm, hit_inc, n_hits, gv, sv, c, nodes.get());
+  seed_kernel<<<nb(n_local), kT, 0, s>>>(hit_ie, hit_kind, hit_pos, hit_nrm, hit_inc, n_local, shard, n_shards, gv, sv,
+                                         c, nodes.get());
   PCR_LAUNCH_CHECK();
   size_t cand_cap = 1u << 20;
   DBuf<Cand> cands(cand_cap, s);
@@ -898,7 +927,7 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
     e.v_done = 0;
     if (e.v_total) stack.push_back(std::move(e));
   };
-  push_range(0, n_hits);
+  push_range(0, n_local);
 
   while (!stack.empty()) {
     StackEntry& top = stack.back();
@@ -989,7 +1018,8 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
   uint32_t nk = 0;
   {
     KTimer kt(ctx, "kappa_select");
-    kappa_select(ctx, grid, cands, n_cands, nodes.get(), L, c.kappa, kept, nk);
+    kappa_select(ctx, grid, cands, n_cands, nodes.get(), L, c.kappa, kept, nk, want_keys ? &out.keys : nullptr,
+                 want_keys ? &out.hash : nullptr);
   }
   out.n = nk;
   const size_t m = nk ? nk : 1;
@@ -1024,6 +1054,219 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
   PCR_CUDA(cudaStreamSynchronize(s));
   stats.walk_cells += ws[0];
   stats.walk_ies += ws[1];
+}
+
+// ---- sharded propagation: candidate rows and the global kappa merge ---------
+namespace {
+
+__global__ void pack_rows_kernel(uint32_t n, uint32_t stride, uint32_t tx_index, const uint32_t* __restrict__ rx_id,
+                                 const uint32_t* __restrict__ n_inter, const double* __restrict__ rx_pos,
+                                 const double* __restrict__ length, const uint8_t* __restrict__ kind,
+                                 const double* __restrict__ pos, const uint32_t* __restrict__ label,
+                                 const double* __restrict__ nrm, const uint32_t* __restrict__ ie,
+                                 const uint32_t* __restrict__ edge, const uint64_t* __restrict__ keys,
+                                 const uint64_t* __restrict__ hash, uint8_t* __restrict__ rows) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  uint8_t* r = rows + static_cast<size_t>(k) * cand_row_bytes(stride);
+  CandRowHead h;
+  for (int q = 0; q < 4; ++q) h.key[q] = keys[static_cast<size_t>(q) * n + k];
+  h.hash = hash[k];
+  h.tx_index = tx_index;
+  h.rx_id = rx_id[k];
+  h.n_inter = n_inter[k];
+  h.pad0 = 0;
+  for (int a = 0; a < 3; ++a) h.rx_pos[a] = rx_pos[3ull * k + a];
+  h.length = length[k];
+  h.pad1 = 0.0;
+  *reinterpret_cast<CandRowHead*>(r) = h;
+  CandRowLevel* lv = reinterpret_cast<CandRowLevel*>(r + sizeof(CandRowHead));
+  for (uint32_t q = 0; q < stride; ++q) {
+    const size_t j = static_cast<size_t>(k) * stride + q;
+    CandRowLevel l;
+    for (int a = 0; a < 3; ++a) {
+      l.pos[a] = pos[3 * j + a];
+      l.nrm[a] = nrm[3 * j + a];
+    }
+    l.label = label[j];
+    l.ie = ie[j];
+    l.edge = edge[j];
+    l.kind = kind[j];
+    lv[q] = l;
+  }
+}
+
+__device__ __forceinline__ const CandRowHead& row_head(const uint8_t* rows, size_t bytes, uint32_t i) {
+  return *reinterpret_cast<const CandRowHead*>(rows + static_cast<size_t>(i) * bytes);
+}
+
+// word q of every row's key (q = 4: tx index), through perm
+__global__ void row_word_kernel(const uint8_t* __restrict__ rows, size_t bytes, const uint32_t* __restrict__ perm,
+                                uint32_t n, int q, uint64_t* __restrict__ out) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const CandRowHead& h = row_head(rows, bytes, perm[k]);
+  out[k] = q < 4 ? h.key[q] : q == 4 ? static_cast<uint64_t>(h.tx_index) : h.hash;
+}
+
+__device__ bool same_row_group(const uint8_t* rows, size_t bytes, uint32_t a, uint32_t b) {
+  const CandRowHead& x = row_head(rows, bytes, a);
+  const CandRowHead& y = row_head(rows, bytes, b);
+  if (x.tx_index != y.tx_index || x.rx_id != y.rx_id || x.n_inter != y.n_inter) return false;
+  const CandRowLevel* lx = reinterpret_cast<const CandRowLevel*>(rows + static_cast<size_t>(a) * bytes + sizeof(CandRowHead));
+  const CandRowLevel* ly = reinterpret_cast<const CandRowLevel*>(rows + static_cast<size_t>(b) * bytes + sizeof(CandRowHead));
+  for (uint32_t q = 0; q < x.n_inter; ++q)
+    if (lx[q].label != ly[q].label) return false;
+  return true;
+}
+
+// rows in (tx, hash, key) order: run heads, with every non-head checked to be in the
+// same (tx, rx, labels) group as its predecessor (a hash collision is an error)
+__global__ void row_rank_kernel(const uint8_t* __restrict__ rows, size_t bytes, const uint32_t* __restrict__ perm,
+                                uint32_t n, uint32_t* __restrict__ run_start, int* __restrict__ collision) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  bool head = k == 0;
+  if (!head) {
+    const CandRowHead& a = row_head(rows, bytes, perm[k]);
+    const CandRowHead& b = row_head(rows, bytes, perm[k - 1]);
+    head = a.tx_index != b.tx_index || a.hash != b.hash;
+    if (!head && !same_row_group(rows, bytes, perm[k], perm[k - 1])) *collision = 1;
+  }
+  run_start[k] = head ? k : 0;
+}
+
+__global__ void unpack_rows_kernel(const uint8_t* __restrict__ rows, uint32_t stride, const uint32_t* __restrict__ perm,
+                                   const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, uint32_t n,
+                                   CandOut o, uint32_t* __restrict__ per_tx) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n || !flag[k]) return;
+  const size_t bytes = cand_row_bytes(stride);
+  const uint8_t* r = rows + static_cast<size_t>(perm[k]) * bytes;
+  const CandRowHead& h = *reinterpret_cast<const CandRowHead*>(r);
+  const CandRowLevel* lv = reinterpret_cast<const CandRowLevel*>(r + sizeof(CandRowHead));
+  const uint32_t d = pos[k];
+  o.rx_id[d] = h.rx_id;
+  o.n_inter[d] = h.n_inter;
+  for (int a = 0; a < 3; ++a) o.rx_pos[3ull * d + a] = h.rx_pos[a];
+  o.length[d] = h.length;
+  for (uint32_t q = 0; q < stride; ++q) {
+    const size_t j = static_cast<size_t>(d) * stride + q;
+    for (int a = 0; a < 3; ++a) {
+      o.pos[3 * j + a] = lv[q].pos[a];
+      o.nrm[3 * j + a] = lv[q].nrm[a];
+    }
+    o.label[j] = lv[q].label;
+    o.ie[j] = lv[q].ie;
+    o.edge[j] = lv[q].edge;
+    o.kind[j] = static_cast<uint8_t>(lv[q].kind);
+  }
+  atomicAdd(per_tx + h.tx_index, 1u);
+}
+
+}  // namespace
+
+void pack_cand_rows(Ctx& ctx, const CandDev& c, uint32_t tx_index, uint8_t* rows) {
+  if (!c.n) return;
+  if (!c.keys.get() || !c.hash.get()) throw Error(1, "trace: candidate rows need DFS keys");
+  count_launch();
+  pack_rows_kernel<<<nb(c.n), kT, 0, ctx.stream>>>(c.n, c.stride, tx_index, c.rx_id.get(), c.n_inter.get(),
+                                                   c.rx_pos.get(), c.length.get(), c.kind.get(), c.pos.get(),
+                                                   c.label.get(), c.nrm.get(), c.ie.get(), c.edge.get(),
+                                                   c.keys.get(), c.hash.get(), rows);
+  PCR_LAUNCH_CHECK();
+}
+
+// Global first-kappa over every shard's rows, concatenated in any order: the rows are
+// put in (tx, DFS key) order — the reference's emission order per TX — and grouped by
+// (tx, rx, label sequence); the first kappa of each group survive. Every shard kept the
+// first kappa of its own subset of each group, a superset of its share of the global
+// first kappa (T9), so the result equals the unsharded propagate. Output: all TXs'
+// kept candidates in (tx, key) order and the number per TX.
+void kappa_merge_rows(Ctx& ctx, const uint8_t* rows, uint64_t n64, uint32_t stride, int kappa, uint32_t n_tx,
+                      CandDev& out, std::vector<uint32_t>& per_tx) {
+  cudaStream_t s = ctx.stream;
+  per_tx.assign(n_tx, 0);
+  out.n = 0;
+  out.stride = stride;
+  if (n64 > 0xffffffffull) throw Error(PCR_ERR_NOMEM, "trace: too many candidate rows");
+  const uint32_t n = static_cast<uint32_t>(n64);
+  const size_t bytes = cand_row_bytes(stride);
+  const size_t m = n ? n : 1, ms = m * stride;
+  out.rx_id.alloc(m, s);
+  out.n_inter.alloc(m, s);
+  out.rx_pos.alloc(3 * m, s);
+  out.length.alloc(m, s);
+  out.kind.alloc(ms, s);
+  out.pos.alloc(3 * ms, s);
+  out.label.alloc(ms, s);
+  out.nrm.alloc(3 * ms, s);
+  out.ie.alloc(ms, s);
+  out.edge.alloc(ms, s);
+  if (!n) return;
+  KTimer kt(ctx, "kappa_merge");
+  DBuf<uint32_t> perm_key(n, s), perm(n, s);
+  DBuf<uint64_t> tmp(n, s);
+  iota_u32(perm_key.get(), n, s);
+  // LSD: key words least significant first, then the TX index
+  const int order[5] = {3, 2, 1, 0, 4};
+  for (int w : order) {
+    count_launch();
+    row_word_kernel<<<nb(n), kT, 0, s>>>(rows, bytes, perm_key.get(), n, w, tmp.get());
+    PCR_LAUNCH_CHECK();
+    radix_sort_pairs(tmp.get(), perm_key.get(), n, 0, w == 4 ? 32 : 64, s);
+  }
+  // group order (tx, hash, key): stable sorts of the key order by hash, then by tx
+  PCR_CUDA(cudaMemcpyAsync(perm.get(), perm_key.get(), n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+  for (int w : {5, 4}) {
+    count_launch();
+    row_word_kernel<<<nb(n), kT, 0, s>>>(rows, bytes, perm.get(), n, w, tmp.get());
+    PCR_LAUNCH_CHECK();
+    radix_sort_pairs(tmp.get(), perm.get(), n, 0, w == 4 ? 32 : 64, s);
+  }
+  DBuf<uint32_t> run_start(n, s);
+  DBuf<int> collision(1, s);
+  PCR_CUDA(cudaMemsetAsync(collision.get(), 0, sizeof(int), s));
+  count_launch();
+  row_rank_kernel<<<nb(n), kT, 0, s>>>(rows, bytes, perm.get(), n, run_start.get(), collision.get());
+  PCR_LAUNCH_CHECK();
+  {
+    const uint32_t nblk = (n + 1023) / 1024;
+    DBuf<uint32_t> bm(nblk, s);
+    count_launch();
+    run_max_block_kernel<<<nblk, 1024, 0, s>>>(run_start.get(), n, bm.get());
+    if (nblk > 1) {
+      count_launch();
+      max_scan_small_kernel<<<1, 1, 0, s>>>(bm.get(), nblk);
+      count_launch();
+      run_max_fix_kernel<<<nblk, 1024, 0, s>>>(run_start.get(), n, bm.get());
+    }
+    PCR_LAUNCH_CHECK();
+  }
+  DBuf<uint8_t> keep(n, s);
+  count_launch();
+  keep_kernel<<<nb(n), kT, 0, s>>>(run_start.get(), perm.get(), n, kappa, keep.get());
+  DBuf<uint32_t> flag(n, s), pos(n, s), tot(1, s);
+  count_launch();
+  keep_flags_in_order_kernel<<<nb(n), kT, 0, s>>>(keep.get(), perm_key.get(), n, flag.get());
+  PCR_LAUNCH_CHECK();
+  exclusive_scan_u32(flag.get(), pos.get(), n, tot.get(), s);
+  DBuf<uint32_t> cnt(n_tx ? n_tx : 1, s);
+  PCR_CUDA(cudaMemsetAsync(cnt.get(), 0, (n_tx ? n_tx : 1) * sizeof(uint32_t), s));
+  CandOut co{stride,         out.rx_id.get(), out.rx_pos.get(), out.length.get(), out.n_inter.get(),
+             out.kind.get(), out.pos.get(),   out.label.get(),  out.nrm.get(),    out.ie.get(),
+             out.edge.get()};
+  count_launch();
+  unpack_rows_kernel<<<nb(n), kT, 0, s>>>(rows, stride, perm_key.get(), flag.get(), pos.get(), n, co, cnt.get());
+  PCR_LAUNCH_CHECK();
+  int coll = 0;
+  uint32_t n_out = 0;
+  d2h(&coll, collision.get(), 1, s);
+  d2h(&n_out, tot.get(), 1, s);
+  if (n_tx) d2h(per_tx.data(), cnt.get(), n_tx, s);
+  PCR_CUDA(cudaStreamSynchronize(s));
+  if (coll) throw Error(4, "trace: group hash collision in kappa selection");
+  out.n = n_out;
 }
 
 // ---- C-ABI adapters ---------------------------------------------------------------------

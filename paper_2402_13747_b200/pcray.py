@@ -63,6 +63,13 @@ def lib():
         L.pcr_refine_batch.argtypes = [vp, vp, vp, pp(abi.Paths), pp(abi.RefineParams), pp(pp(abi.Outcomes))]
         L.pcr_run_pipeline_on_scene.argtypes = [vp, pp(abi.SceneDesc), pp(abi.RunConfig), pp(pp(abi.Summary))]
         L.pcr_run_pipeline_device.argtypes = [vp, vp, pp(abi.RunConfig), pp(pp(abi.Summary))]
+        L.pcr_shard_trace.argtypes = [vp, vp, pp(abi.RunConfig), C.c_uint32, C.c_uint32, pp(C.c_uint64),
+                                      pp(C.c_uint64)]
+        L.pcr_shard_rows.argtypes = [vp, vp]
+        L.pcr_shard_refine.argtypes = [vp, vp, vp, C.c_uint64, pp(C.c_uint64), pp(C.c_uint64)]
+        L.pcr_shard_outcomes.argtypes = [vp, vp]
+        L.pcr_shard_stats_get.argtypes = [vp, pp(abi.ShardStats)]
+        L.pcr_shard_finish.argtypes = [vp, vp, C.c_uint64, pp(abi.ShardStats), pp(pp(abi.Summary))]
         L.pcr_stream.restype = vp
         L.pcr_stream.argtypes = [vp]
         L.pcr_set_profiling.argtypes = [vp, C.c_int]
@@ -88,7 +95,8 @@ EXPORTED_SYMBOLS = [
     "pcr_free_grid_host", "pcr_transmission_phase", "pcr_propagate", "pcr_cone_trace_batch",
     "pcr_segment_visible_batch", "pcr_refine_batch", "pcr_run_pipeline_on_scene", "pcr_config_hash",
     "pcr_run_config_defaults", "pcr_free_paths", "pcr_free_initial_hits", "pcr_free_outcomes",
-    "pcr_free_summary", "pcr_free_receptions",
+    "pcr_free_summary", "pcr_free_receptions", "pcr_run_pipeline_device", "pcr_shard_trace", "pcr_shard_rows",
+    "pcr_shard_refine", "pcr_shard_outcomes", "pcr_shard_stats_get", "pcr_shard_finish",
 ]
 
 
@@ -290,6 +298,48 @@ def run_pipeline_device(scene: DeviceScene, config: RunConfig | None = None) -> 
     config = config or default_run_config()
     out = C.POINTER(abi.Summary)()
     scene.ctx.check(lib().pcr_run_pipeline_device(scene.ctx.handle, scene.handle, C.byref(config), C.byref(out)))
+    try:
+        return abi.summary_to_dict(out.contents)
+    finally:
+        lib().pcr_free_summary(out)
+
+
+# ---- sharded pipeline (one process per GPU; orchestration in shard.py) ---------------------------
+def shard_trace(scene: DeviceScene, config: RunConfig, shard: int, n_shards: int) -> tuple[int, int]:
+    """pcr_shard_trace: validate, build_grid, transmission, this shard's propagate -> (rows, row bytes)."""
+    n, b = C.c_uint64(), C.c_uint64()
+    scene.ctx.check(lib().pcr_shard_trace(scene.ctx.handle, scene.handle, C.byref(config), shard, n_shards,
+                                          C.byref(n), C.byref(b)))
+    return n.value, b.value
+
+
+def shard_rows(ctx: Context, dst_ptr: int) -> None:
+    ctx.check(lib().pcr_shard_rows(ctx.handle, C.c_void_p(dst_ptr)))
+
+
+def shard_refine(scene: DeviceScene, rows_ptr: int, n_rows: int) -> tuple[int, int]:
+    """pcr_shard_refine: global kappa over every shard's rows, refine this shard's share -> (rows, bytes)."""
+    n, b = C.c_uint64(), C.c_uint64()
+    scene.ctx.check(lib().pcr_shard_refine(scene.ctx.handle, scene.handle, C.c_void_p(rows_ptr or None), n_rows,
+                                           C.byref(n), C.byref(b)))
+    return n.value, b.value
+
+
+def shard_outcomes(ctx: Context, dst_ptr: int) -> None:
+    ctx.check(lib().pcr_shard_outcomes(ctx.handle, C.c_void_p(dst_ptr)))
+
+
+def shard_stats(ctx: Context) -> np.ndarray:
+    st = abi.ShardStats()
+    ctx.check(lib().pcr_shard_stats_get(ctx.handle, C.byref(st)))
+    return np.array([getattr(st, f) for f in abi.SHARD_STATS_FIELDS], dtype=np.uint64)
+
+
+def shard_finish(ctx: Context, rows_ptr: int, n_rows: int, totals) -> dict:
+    """pcr_shard_finish: every shard's outcome rows + summed stats -> the RunSummary."""
+    st = abi.ShardStats(*[int(x) for x in totals])
+    out = C.POINTER(abi.Summary)()
+    ctx.check(lib().pcr_shard_finish(ctx.handle, C.c_void_p(rows_ptr or None), n_rows, C.byref(st), C.byref(out)))
     try:
         return abi.summary_to_dict(out.contents)
     finally:
