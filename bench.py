@@ -163,7 +163,7 @@ def reference_arm(args, rank, world):
               f"{counted['candidates']} candidates; {rays} launched rays per step")
     line = {"metric": METRIC, "value": value, "unit": "Mrays/s", "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C2 synthetic office (SURVEY.md §8.0)", "points": scene.n_points,
                        "tx": 1, "rx": 64, "max_interactions": cfg.run["max_interactions"],
                        "max_diffractions": cfg.run["max_diffractions"], "task_stride": stride},
@@ -179,7 +179,7 @@ def b200_arm(args, rank, world, local_rank):
     import numpy as np
     import torch
 
-    from paper_2402_13747_b200 import abi, pcray, scenes
+    from paper_2402_13747_b200 import abi, pcray, scenes, shard
 
     torch.cuda.set_device(local_rank)
     dist = None
@@ -237,21 +237,34 @@ def b200_arm(args, rank, world, local_rank):
         pcray.set_profiling(False, ctx)
         return ms, outs, launches, (t1[0] - t0[0], t1[1] - t0[1]), kt
 
+    # N = 1: the whole pipeline on one device. N > 1: one shard per rank (
+    # shard.py): the same scene and total work, split by initial hit and by candidate,
+    # rows exchanged over NCCL — strong scaling, rank 0 holds the RunSummary.
+    if world > 1:
+        def step():
+            return shard.run_pipeline_sharded(ds, conf)
+    else:
+        def step():
+            return pcray.run_pipeline_device(ds, conf)
+
     for _ in range(args.warmup):
-        pcray.run_pipeline_device(ds, conf)
+        step()
     barrier()
     with ClockSampler(local_rank) as clocks:
         barrier()
-        ms, outs, launches, _, ktimes = timed_steps(lambda: pcray.run_pipeline_device(ds, conf), args.steps,
-                                                   profile=True)
+        ms, outs, launches, _, ktimes = timed_steps(step, args.steps, profile=True)
         barrier()
     step_ms = max_over_ranks(sum(ms)) / args.steps
+    launches = int(sum_over_ranks(launches))
     s0 = outs[-1]
-    rays = s0["transmission_rays"] + s0["cone_traces"]
-    total_rays = sum_over_ranks(rays * args.steps)
-    value = total_rays / (step_ms * args.steps * 1e-3) / 1e6
-    exact_per_s = sum_over_ranks(s0["exact_paths"] * args.steps) / (step_ms * args.steps * 1e-3)
-    cand_per_s = sum_over_ranks(s0["coarse_paths"] * args.steps) / (step_ms * args.steps * 1e-3)
+    if world > 1:
+        own = dict(zip(abi.SHARD_STATS_FIELDS, (int(x) for x in pcray.shard_stats(ctx))))
+    else:
+        own = s0
+    rays = s0["transmission_rays"] + s0["cone_traces"] if rank == 0 else 0
+    value = rays / (step_ms * 1e-3) / 1e6
+    exact_per_s = (s0["exact_paths"] if rank == 0 else 0) / (step_ms * 1e-3)
+    cand_per_s = (s0["coarse_paths"] if rank == 0 else 0) / (step_ms * 1e-3)
     clk = clocks.summary()
 
     # e2e: host buffers (pinned), copies inside the timed region, through the public C-ABI call
@@ -263,23 +276,28 @@ def b200_arm(args, rank, world, local_rank):
         pin[name] = t.numpy()
     host_scene = abi.Scene(pin["position"], pin["normal"], pin["label"], pin["edges"], pin["edge_label"], pin["tx"],
                            pin["tx_id"], pin["rx"], pin["rx_id"], scene.carrier_frequency_hz)
-    for _ in range(1):
-        pcray.run_pipeline_on_scene(host_scene, conf, ctx)
+    if world > 1:
+        def e2e_step():  # scene upload from pinned host memory + sharded run + result on rank 0's host
+            return shard.run_pipeline_sharded(pcray.DeviceScene(host_scene, ctx), conf)
+    else:
+        def e2e_step():
+            return pcray.run_pipeline_on_scene(host_scene, conf, ctx)
+    e2e_step()
     barrier()
-    e_ms, e_outs, _, (h2d, d2h), _ = timed_steps(lambda: pcray.run_pipeline_on_scene(host_scene, conf, ctx),
-                                                 args.steps)
+    e_ms, e_outs, _, (h2d, d2h), _ = timed_steps(e2e_step, args.steps)
     e_step = max_over_ranks(sum(e_ms)) / args.steps
-    e_value = sum_over_ranks(rays * args.steps) / (e_step * args.steps * 1e-3) / 1e6
+    e_value = rays / (e_step * 1e-3) / 1e6
 
     # parity self-check of the timed runs: identical summaries step to step
     for s in outs + e_outs:
-        assert s["exact_paths"] == s0["exact_paths"] and s["coarse_paths"] == s0["coarse_paths"]
+        if s is not None:
+            assert s["exact_paths"] == s0["exact_paths"] and s["coarse_paths"] == s0["coarse_paths"]
 
     peaks, peaks_kind = measured_peaks()
     fp64 = pcray.fp64_probe(ctx)
     dom = max(ktimes.items(), key=lambda kv: kv[1][0]) if ktimes else ("none", (0.0, 1))
     mean_depth = 3.0
-    rl = roofline(dom[0], dom[1][0] / args.steps, max(1, dom[1][1] // args.steps), s0, mean_depth, peaks,
+    rl = roofline(dom[0], dom[1][0] / args.steps, max(1, dom[1][1] // args.steps), own, mean_depth, peaks,
                   peaks_kind, fp64)
     total_k = sum(v[0] for v in ktimes.values())
     shares = {k: round(v[0] / total_k, 4) for k, v in sorted(ktimes.items(), key=lambda kv: -kv[1][0])}
@@ -303,13 +321,14 @@ def b200_arm(args, rank, world, local_rank):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C2 synthetic office (SURVEY.md §8.0; BASELINE configs[1])",
                        "points": scene.n_points, "tx": int(len(scene.tx)), "rx": int(len(scene.rx)),
                        "edges": int(len(scene.edges)), "max_interactions": cfg.run["max_interactions"],
                        "max_diffractions": cfg.run["max_diffractions"], "kappa": conf.kappa,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"{world} shards: initial hits and candidates split cyclically, "
+                                       "rows all-gathered over NCCL" if world > 1 else "single GPU"),
                        "l2": "flushed (256 MB write) before every timed step"},
             "rays_per_step": rays, "exact_paths_per_s": exact_per_s, "candidates_refined_per_s": cand_per_s,
             "exact_paths": s0["exact_paths"], "coarse_paths": s0["coarse_paths"],

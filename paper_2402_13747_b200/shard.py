@@ -37,7 +37,11 @@ def shard_indices(n: int, shard: int, world: int) -> range:
 
 
 def all_gather_bytes(buf: torch.Tensor, group=None) -> torch.Tensor:
-    """Concatenation, in rank order, of every rank's 1-D uint8 tensor (sizes may differ)."""
+    """Concatenation, in rank order, of every rank's 1-D uint8 tensor (sizes may differ).
+    NCCL moves device tensors directly; under gloo a device tensor is staged through
+    host memory (gloo's all-gather is host-side)."""
+    if buf.is_cuda and dist.get_backend(group) == "gloo":
+        return all_gather_bytes(buf.cpu(), group).to(buf.device)
     world = dist.get_world_size(group)
     dev = buf.device
     size = torch.tensor([buf.numel()], dtype=torch.int64, device=dev)
@@ -56,6 +60,8 @@ def all_gather_bytes(buf: torch.Tensor, group=None) -> torch.Tensor:
 
 def sum_stats(stats: np.ndarray, group=None, device=None) -> np.ndarray:
     """Element-wise sum of every rank's pcr_shard_stats counters."""
+    if dist.get_backend(group) == "gloo":
+        device = None
     t = torch.tensor(stats.astype(np.int64), dtype=torch.int64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t.cpu().numpy().astype(np.uint64)

@@ -87,3 +87,55 @@ def test_shard_errors(gpu):
     sc = pcray.DeviceScene(make_scene(box_room((2, 2, 2), 0.1), tx=[(0.6, 0.7, 0.9)], rx=[(1.3, 1.2, 1.1)]), ctx)
     with pytest.raises(pcray.PcrError, match="shard: index out of range"):
         pcray.shard_trace(sc, abi.default_run_config(max_interactions=1), 2, 2)
+
+
+def _rank(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    # gloo keeps the exchange on the host: the ranks share one GPU but never wait on
+    # each other's kernels (each shard's kernels run to completion before a collective)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        scene, c = scenes.build_scene("C1")
+        ds = pcray.DeviceScene(scene, pcray.Context(0))
+        s = shard.run_pipeline_sharded(ds, abi.default_run_config(**c.run))
+        q.put((rank, None if s is None else {k: s[k] for k in COUNTS + ["paths"]}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_run_pipeline_sharded_distributed(gpu):
+    """shard.run_pipeline_sharded itself under torch.distributed (world 2)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[1] is None
+    scene, c = scenes.build_scene("C1")
+    ref = pcray.run_pipeline_on_scene(scene, abi.default_run_config(**c.run))
+    got = res[0]
+    for k in COUNTS:
+        assert got[k] == ref[k], k
+    for k, v in ref["paths"].items():
+        a, b = np.ascontiguousarray(got["paths"][k]), np.ascontiguousarray(v)
+        if a.dtype == np.float64:
+            a, b = a.view(np.uint64), b.view(np.uint64)
+        assert np.array_equal(a, b), k
