@@ -36,6 +36,11 @@ struct GridView {
   const uint32_t* ie_edge;
   const uint32_t* ie_rx;
   const uint32_t* point_indices;
+  // refinement scan records (built per refine call): {sphere centre, label | meta << 32};
+  // rr_radius is every IE's sphere radius when rr_uniform (as build_grid makes them)
+  const double4* ie_rr = nullptr;
+  double rr_radius = 0.0;
+  int rr_uniform = 0;
 };
 
 // Device-resident Scene (scene.hpp:38-46).

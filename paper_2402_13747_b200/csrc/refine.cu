@@ -7,7 +7,11 @@
 // Shortcut (bit-exact): when no trial step is accepted the state is unchanged, so
 // every remaining iteration repeats the same computation and the outcome is
 // not_converged; the kernel stops there instead of spinning to rho.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "host_alloc.hpp"
@@ -89,6 +93,8 @@ __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, c
     uint32_t best_ie = kNoIe;
     double best_t = 1.7976931348623157e308;
     Reproj best;  // only for a non-planar winner; planar winners are rebuilt below
+    long long c_num = 0x7ff8dead7ff8deadll, c_dn = 0x7ff8dead7ff8deadll;  // (num, dn) bits of the cached t*
+    double c_t = 0.0;
     // one flat loop over (cell z→y→x, IE in cell order): lanes of a warp stay in the
     // same loop body whatever their cells' occupancy
     int x = lo[0], y = lo[1], z = lo[2];
@@ -108,20 +114,59 @@ __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, c
         continue;
       }
       const uint32_t ie = i++;
-      // the three filters are pure predicates: cheapest first
-      if (same != (g.ie_label[ie] == label)) continue;
-      if ((g.ie_meta[ie] & 3u) != kSurface) continue;
-      const double4 sc4 = g.ie_sc[ie];
-      if (!norm_le(ld3(sc4) - predicted, radius + sc4.w)) continue;
+      // one 32-byte record answers the three filters (pure predicates, cheapest first)
+      const double4 r4 = g.ie_rr[ie];
+      const uint64_t lm = static_cast<uint64_t>(__double_as_longlong(r4.w));
+      if (same != (static_cast<uint32_t>(lm) == label)) continue;
+      if (((lm >> 32) & 3u) != kSurface) continue;
+      const V3 sc = ld3(r4);
+      const double rad = g.rr_uniform ? g.rr_radius : g.ie_sc[ie].w;
+      if (!norm_le(sc - predicted, radius + rad)) continue;
       ++n_march;  // counts the reference's march_segment call
       // march_segment's window (surface.cpp:64-72): every hit it returns lies at
       // t >= t_lo, so a window starting at or past the best t cannot win (strict <)
-      const double t_center = dot(ld3(sc4) - prev, dir);
-      const double t_lo = smax(0.0, t_center - sc4.w);
+      const double t_center = dot(sc - prev, dir);
+      const double t_lo = smax(0.0, t_center - rad);
       if (t_lo >= best_t) continue;
-      if (ie_planar(g, ie)) {
-        double t;
-        if (!planar_march_t(prev, dir, ie, g, t_lo, t_center + sc4.w, t)) continue;
+      if ((lm >> 34) & 1u) {
+        // planar march_segment (surface.cpp:74-106), reordered: a hit's distance is the
+        // snap t* when t* falls in the window, so such a window cannot win once
+        // t* >= best_t and the two endpoint tests are skipped. Coplanar IEs (same
+        // normal and plane offset bits, e.g. the IEs of one wall) share t*: the
+        // division is done once per plane.
+        const double t_hi = t_center + rad;
+        if (t_hi <= t_lo) continue;
+        const V3 pp = ld3(g.ie_pp[ie]), pn = ld3(g.ie_pn[ie]);
+        const double dn = dot(dir, pn);
+        const bool snap = fabs(dn) > 1e-12;
+        double t_star = 0.0;
+        if (snap) {
+          const double num = dot(pp - prev, pn);
+          const long long nb_ = __double_as_longlong(num), db_ = __double_as_longlong(dn);
+          if (nb_ != c_num || db_ != c_dn) {
+            c_num = nb_;
+            c_dn = db_;
+            c_t = num / dn;
+          }
+          t_star = c_t;
+        }
+        const bool in_win = snap && t_star >= t_lo && t_star <= t_hi;
+        if (in_win && t_star >= best_t) continue;
+        const double eps = g.hit_eps;
+        double tc;
+        const double f = dot((prev + t_lo * dir) - pp, pn);
+        if (fabs(f) <= eps) {
+          tc = t_lo;
+        } else {
+          const double f_hi = dot((prev + t_hi * dir) - pp, pn);
+          if (f * f_hi < 0.0)
+            tc = 0.5 * (t_lo + t_hi);
+          else if (fabs(f_hi) <= eps)
+            tc = t_hi;
+          else
+            continue;
+        }
+        const double t = in_win ? t_star : tc;
         if (t >= best_t) continue;
         best_t = t;
         best_ie = ie;
@@ -255,14 +300,29 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
 // rho, so a thread that finishes a path takes the next one instead of idling until
 // the slowest lane of its warp is done.
 constexpr int kRefineThreads = 128;
+__device__ unsigned long long* g_refine_dbg = nullptr;
 __global__ void __launch_bounds__(kRefineThreads, 4) refine_kernel(CandIn in, uint32_t n, GridView g, SceneView s,
                                                                    double delta, int rho, double step_size, RefOut o,
-                                                                   uint32_t* next_cand) {
+                                                                   uint32_t* next_cand, int rev) {
+  uint32_t done = 0;
+  unsigned long long t_start = 0;
+  if (g_refine_dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   for (;;) {
     const uint32_t idx = atomicAdd(next_cand, 1u);
     if (idx >= n) break;
     // this shard's candidates are first, first + step, ... (SURVEY 8e round-robin)
-    refine_one(in.first + idx * in.step, in, g, s, delta, rho, step_size, o);
+    // list order by default (measured faster than back to front, PCR_REFINE_REV=1:
+    // neighbours in DFS order are similar paths, so a warp's lanes diverge less)
+    refine_one(in.first + (rev ? n - 1 - idx : idx) * in.step, in, g, s, delta, rho, step_size, o);
+    ++done;
+  }
+  if (g_refine_dbg) {  // development trace (PCR_REFINE_TRACE): per-thread finish time, paths
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    g_refine_dbg[3 * tid] = t_start;
+    g_refine_dbg[3 * tid + 1] = t;
+    g_refine_dbg[3 * tid + 2] = done;
   }
 }
 
@@ -318,8 +378,10 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
     atomicAdd(o.stats + 1, static_cast<unsigned long long>(n_march));
   };
   // Brent cycle detection on the post-iteration state
-  Snapshot saved;
+  Snapshot saved, last[2];  // Brent's saved state; the states 1 and 2 iterations back
   take_snapshot(saved, nd, d);
+  last[0] = saved;
+  last[1] = saved;
   int power = 1, lam = 0;
   bool stalled = false;
   for (; iter < rho; ++iter) {
@@ -406,12 +468,16 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
     }
     for (int q = 0; q < d; ++q) pts[q] = node_point(nd[q], nd[q].p0, nd[q].p1);
     f = chain_len(tx, pts, d, rx);
-    if (same_snapshot(saved, nd, d)) {
-      stalled = true;  // periodic trajectory: never converges (see Snapshot)
+    // periodic trajectory: never converges (see Snapshot). Periods 1 and 2 are caught
+    // at once, longer ones by Brent's doubling schedule.
+    const int slot = iter & 1;
+    if (same_snapshot(last[slot ^ 1], nd, d) || same_snapshot(last[slot], nd, d) || same_snapshot(saved, nd, d)) {
+      stalled = true;
       break;
     }
+    take_snapshot(last[slot], nd, d);
     if (++lam == power) {
-      take_snapshot(saved, nd, d);
+      saved = last[slot];
       power <<= 1;
       lam = 0;
     }
@@ -448,6 +514,25 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
   o.has_path[k] = 1;
 }
 
+// refinement scan records: {sphere centre, label | meta << 32}; flags any IE whose
+// sphere radius differs (bitwise) from the first one's
+__global__ void refine_records_kernel(GridView g, double4* __restrict__ rr, int* __restrict__ nonuniform) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n_ies) return;
+  const double4 sc = g.ie_sc[i];
+  const uint64_t lm = static_cast<uint64_t>(g.ie_label[i]) | (static_cast<uint64_t>(g.ie_meta[i]) << 32);
+  rr[i] = make_double4(sc.x, sc.y, sc.z, __longlong_as_double(static_cast<long long>(lm)));
+  if (__double_as_longlong(sc.w) != __double_as_longlong(g.ie_sc[0].w)) *nonuniform = 1;
+}
+
+int rev_order() {
+  static const int r = [] {
+    const char* e = std::getenv("PCR_REFINE_REV");
+    return e ? std::atoi(e) : 0;
+  }();
+  return r;
+}
+
 unsigned nb(uint64_t n, unsigned t) { return static_cast<unsigned>((n + t - 1) / t ? (n + t - 1) / t : 1); }
 
 }  // namespace
@@ -474,6 +559,25 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
   const uint32_t step = in.step ? in.step : 1;
   const uint32_t n_sub = in.n > in.first ? (in.n - in.first + step - 1) / step : 0;
   if (!n_sub) return;
+  GridView gv = grid.view();
+  DBuf<double4> rr(grid.n_ies ? grid.n_ies : 1, s);
+  {
+    DBuf<int> nonuni(1, s);
+    PCR_CUDA(cudaMemsetAsync(nonuni.get(), 0, sizeof(int), s));
+    if (grid.n_ies) {
+      count_launch();
+      refine_records_kernel<<<nb(grid.n_ies, 256), 256, 0, s>>>(gv, rr.get(), nonuni.get());
+      PCR_LAUNCH_CHECK();
+    }
+    int h = 0;
+    d2h(&h, nonuni.get(), 1, s);
+    double r0 = 0.0;
+    if (grid.n_ies) d2h(&r0, &grid.sc.get()->w, 1, s);
+    PCR_CUDA(cudaStreamSynchronize(s));
+    gv.ie_rr = rr.get();
+    gv.rr_uniform = grid.n_ies && !h;
+    gv.rr_radius = r0;
+  }
   CandIn ci{in.first, step, in.stride, in.tx, in.rx, in.n_inter, in.kind, in.pos, in.label, in.nrm, in.edge, in.coarse_length};
   DBuf<unsigned long long> stats(2, s);
   DBuf<uint32_t> next(1, s);
@@ -489,8 +593,51 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     PCR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, kRefineThreads, 0));
     const uint64_t want = (static_cast<uint64_t>(n_sub) + kRefineThreads - 1) / kRefineThreads;
     const uint64_t cap = static_cast<uint64_t>(ctx.sm_count) * (per_sm > 0 ? per_sm : 1);
-    refine_kernel<<<static_cast<unsigned>(want < cap ? want : cap), kRefineThreads, 0, s>>>(
-        ci, n_sub, grid.view(), scene.view(), p.delta, p.rho, p.step_size, ro, next.get());
+    const unsigned grid_n = static_cast<unsigned>(want < cap ? want : cap);
+    const char* trace = std::getenv("PCR_REFINE_TRACE");
+    DBuf<unsigned long long> dbg;
+    unsigned long long t0 = 0;
+    if (trace) {
+      dbg.alloc(3ull * grid_n * kRefineThreads, s);
+      PCR_CUDA(cudaMemsetAsync(dbg.get(), 0, 24ull * grid_n * kRefineThreads, s));
+      unsigned long long* p = dbg.get();
+      PCR_CUDA(cudaMemcpyToSymbolAsync(g_refine_dbg, &p, sizeof(p), 0, cudaMemcpyHostToDevice, s));
+      PCR_CUDA(cudaStreamSynchronize(s));
+      t0 = static_cast<unsigned long long>(std::chrono::duration_cast<std::chrono::nanoseconds>(
+          std::chrono::system_clock::now().time_since_epoch()).count());
+    }
+    refine_kernel<<<grid_n, kRefineThreads, 0, s>>>(
+        ci, n_sub, gv, scene.view(), p.delta, p.rho, p.step_size, ro, next.get(), rev_order());
+    if (trace) {
+      std::vector<unsigned long long> h(3ull * grid_n * kRefineThreads);
+      d2h(h.data(), dbg.get(), h.size(), s);
+      PCR_CUDA(cudaStreamSynchronize(s));
+      unsigned long long* z = nullptr;
+      PCR_CUDA(cudaMemcpyToSymbol(g_refine_dbg, &z, sizeof(z)));
+      if (FILE* f = std::fopen(trace, "wb")) {
+        std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+        std::fclose(f);
+      }
+      // per-candidate iterations, depth, kinds, reason (for cost predictors)
+      std::vector<uint32_t> it(in.n), ni(in.n);
+      std::vector<int32_t> rs(in.n);
+      std::vector<uint8_t> kd(static_cast<size_t>(in.n) * in.stride);
+      d2h(it.data(), out.iters.get(), in.n, s);
+      d2h(rs.data(), out.reason.get(), in.n, s);
+      d2h(ni.data(), in.n_inter, in.n, s);
+      d2h(kd.data(), in.kind, kd.size(), s);
+      PCR_CUDA(cudaStreamSynchronize(s));
+      if (FILE* f = std::fopen((std::string(trace) + ".cand").c_str(), "wb")) {
+        for (uint32_t i = 0; i < in.n; ++i) {
+          uint32_t kinds = 0;
+          for (uint32_t q = 0; q < ni[i] && q < in.stride; ++q) kinds |= (kd[static_cast<size_t>(i) * in.stride + q] & 1u) << q;
+          const uint32_t row[4] = {it[i], ni[i], kinds, static_cast<uint32_t>(rs[i])};
+          std::fwrite(row, sizeof(uint32_t), 4, f);
+        }
+        std::fclose(f);
+      }
+      (void)t0;
+    }
   }
   PCR_LAUNCH_CHECK();
   unsigned long long hs[2];
