@@ -16,6 +16,7 @@
 
 #include "host_alloc.hpp"
 #include "pipeline.hpp"
+#include "sort.cuh"
 #include "stages.cuh"
 #include "trace.cuh"
 
@@ -72,6 +73,52 @@ __device__ __forceinline__ int voxel_floor(double p, double o, double vs) {
   return static_cast<int>(floor((p - o) / vs));
 }
 
+// Planar march_segment (surface.cpp:74-106) of one reprojection candidate, reordered:
+// a hit's distance is the snap t* when t* falls in the window, so such a window
+// cannot win once t* >= best_t and the two endpoint tests are skipped. Coplanar IEs
+// (same normal and plane-offset bits, e.g. the IEs of one wall) share t*: the
+// division is done once per plane (cache c_num, c_dn -> c_t). Returns true and
+// lowers best_t when this IE's hit is strictly nearer.
+__device__ __forceinline__ bool planar_candidate(const V3& prev, const V3& dir, uint32_t ie, const GridView& g,
+                                                 double t_lo, double t_hi, double& best_t, long long& c_num,
+                                                 long long& c_dn, double& c_t) {
+  if (t_hi <= t_lo) return false;
+  const V3 pp = ld3(g.ie_pp[ie]), pn = ld3(g.ie_pn[ie]);
+  const double dn = dot(dir, pn);
+  const bool snap = fabs(dn) > 1e-12;
+  double t_star = 0.0;
+  if (snap) {
+    const double num = dot(pp - prev, pn);
+    const long long nbits = __double_as_longlong(num), dbits = __double_as_longlong(dn);
+    if (nbits != c_num || dbits != c_dn) {
+      c_num = nbits;
+      c_dn = dbits;
+      c_t = num / dn;
+    }
+    t_star = c_t;
+  }
+  const bool in_win = snap && t_star >= t_lo && t_star <= t_hi;
+  if (in_win && t_star >= best_t) return false;
+  const double eps = g.hit_eps;
+  double tc;
+  const double f = dot((prev + t_lo * dir) - pp, pn);
+  if (fabs(f) <= eps) {
+    tc = t_lo;
+  } else {
+    const double f_hi = dot((prev + t_hi * dir) - pp, pn);
+    if (f * f_hi < 0.0)
+      tc = 0.5 * (t_lo + t_hi);
+    else if (fabs(f_hi) <= eps)
+      tc = t_hi;
+    else
+      return false;
+  }
+  const double t = in_win ? t_star : tc;
+  if (t >= best_t) return false;
+  best_t = t;
+  return true;
+}
+
 // reproject (refine.cpp:80-130) with surface_ies_near (:34-52) scanned in place.
 __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, const GridView& g, const SceneView& s,
                           Reproj& out, uint32_t& n_march) {
@@ -83,9 +130,22 @@ __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, c
   const double pc[3] = {predicted.x, predicted.y, predicted.z};
   const double oc[3] = {g.origin.x, g.origin.y, g.origin.z};
   int lo[3], hi[3];
+  bool nb = g.nb_off != nullptr;
+  int cc[3];
   for (int a = 0; a < 3; ++a) {
-    lo[a] = smin(smax(voxel_floor(pc[a] - radius, oc[a], g.voxel_size), 0), g.dims[a] - 1);
-    hi[a] = smin(smax(voxel_floor(pc[a] + radius, oc[a], g.voxel_size), 0), g.dims[a] - 1);
+    const int l = voxel_floor(pc[a] - radius, oc[a], g.voxel_size);
+    const int h = voxel_floor(pc[a] + radius, oc[a], g.voxel_size);
+    lo[a] = smin(smax(l, 0), g.dims[a] - 1);
+    hi[a] = smin(smax(h, 0), g.dims[a] - 1);
+    // the clamped box is the neighbourhood list of cell l + 1 when it spans l..l+2
+    cc[a] = l + 1;
+    nb = nb && h == l + 2 && cc[a] >= 0 && cc[a] < g.dims[a];
+  }
+  uint32_t nb_begin = 0, nb_end = 0;
+  if (nb) {
+    const uint32_t c = linear_index(g, cc[0], cc[1], cc[2]);
+    nb_begin = g.nb_off[c];
+    nb_end = g.nb_off[c + 1];
   }
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   for (int pass = 0; pass < 2; ++pass) {
@@ -97,6 +157,34 @@ __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, c
     double c_t = 0.0;
     // one flat loop over (cell z→y→x, IE in cell order): lanes of a warp stay in the
     // same loop body whatever their cells' occupancy
+    if (nb) {
+      // the box is the 3x3x3 neighbourhood of the predicted point's cell: one
+      // contiguous list of surface-IE records in the same scan order
+      for (uint32_t j = nb_begin; j < nb_end; ++j) {
+        const double4 r4 = g.nb_rec[j];
+        const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r4.w));
+        if (same != (static_cast<uint32_t>(w) == label)) continue;
+        const uint32_t ie = static_cast<uint32_t>(w >> 33);
+        const V3 sc = ld3(r4);
+        const double rad = g.rr_uniform ? g.rr_radius : g.ie_sc[ie].w;
+        if (!norm_le(sc - predicted, radius + rad)) continue;
+        ++n_march;  // counts the reference's march_segment call
+        const double t_center = dot(sc - prev, dir);
+        const double t_lo = smax(0.0, t_center - rad);
+        if (t_lo >= best_t) continue;
+        if ((w >> 32) & 1u) {
+          if (!planar_candidate(prev, dir, ie, g, t_lo, t_center + rad, best_t, c_num, c_dn, c_t)) continue;
+          best_ie = ie;
+        } else {
+          SurfaceHit hit;
+          if (!march_segment(prev, dir, ie, g, s, inf, &hit)) continue;
+          if (hit.distance >= best_t) continue;
+          best_t = hit.distance;
+          best = Reproj{hit.position, hit.normal, g.ie_label[ie]};
+          best_ie = ie;
+        }
+      }
+    } else {
     int x = lo[0], y = lo[1], z = lo[2];
     int4 cell = g.cells[linear_index(g, x, y, z)];
     uint32_t i = static_cast<uint32_t>(cell.x);
@@ -129,46 +217,7 @@ __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, c
       const double t_lo = smax(0.0, t_center - rad);
       if (t_lo >= best_t) continue;
       if ((lm >> 34) & 1u) {
-        // planar march_segment (surface.cpp:74-106), reordered: a hit's distance is the
-        // snap t* when t* falls in the window, so such a window cannot win once
-        // t* >= best_t and the two endpoint tests are skipped. Coplanar IEs (same
-        // normal and plane offset bits, e.g. the IEs of one wall) share t*: the
-        // division is done once per plane.
-        const double t_hi = t_center + rad;
-        if (t_hi <= t_lo) continue;
-        const V3 pp = ld3(g.ie_pp[ie]), pn = ld3(g.ie_pn[ie]);
-        const double dn = dot(dir, pn);
-        const bool snap = fabs(dn) > 1e-12;
-        double t_star = 0.0;
-        if (snap) {
-          const double num = dot(pp - prev, pn);
-          const long long nb_ = __double_as_longlong(num), db_ = __double_as_longlong(dn);
-          if (nb_ != c_num || db_ != c_dn) {
-            c_num = nb_;
-            c_dn = db_;
-            c_t = num / dn;
-          }
-          t_star = c_t;
-        }
-        const bool in_win = snap && t_star >= t_lo && t_star <= t_hi;
-        if (in_win && t_star >= best_t) continue;
-        const double eps = g.hit_eps;
-        double tc;
-        const double f = dot((prev + t_lo * dir) - pp, pn);
-        if (fabs(f) <= eps) {
-          tc = t_lo;
-        } else {
-          const double f_hi = dot((prev + t_hi * dir) - pp, pn);
-          if (f * f_hi < 0.0)
-            tc = 0.5 * (t_lo + t_hi);
-          else if (fabs(f_hi) <= eps)
-            tc = t_hi;
-          else
-            continue;
-        }
-        const double t = in_win ? t_star : tc;
-        if (t >= best_t) continue;
-        best_t = t;
+        if (!planar_candidate(prev, dir, ie, g, t_lo, t_center + rad, best_t, c_num, c_dn, c_t)) continue;
         best_ie = ie;
       } else {
         SurfaceHit hit;
@@ -178,6 +227,7 @@ __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, c
         best = Reproj{hit.position, hit.normal, g.ie_label[ie]};
         best_ie = ie;
       }
+    }
     }
     if (best_ie != kNoIe) {
       if (ie_planar(g, best_ie))  // make_hit's record (surface.cpp:98-106)
@@ -525,6 +575,43 @@ __global__ void refine_records_kernel(GridView g, double4* __restrict__ rr, int*
   if (__double_as_longlong(sc.w) != __double_as_longlong(g.ie_sc[0].w)) *nonuniform = 1;
 }
 
+// neighbourhood lists: count, then fill (cells z->y->x clamped to the grid, surface IEs)
+__global__ void nb_count_kernel(GridView g, uint32_t* __restrict__ cnt) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= g.n_cells) return;
+  const int x = static_cast<int>(c % g.dims[0]), y = static_cast<int>((c / g.dims[0]) % g.dims[1]),
+            z = static_cast<int>(c / (static_cast<uint32_t>(g.dims[0]) * g.dims[1]));
+  uint32_t n = 0;
+  for (int zz = max(z - 1, 0); zz <= min(z + 1, g.dims[2] - 1); ++zz)
+    for (int yy = max(y - 1, 0); yy <= min(y + 1, g.dims[1] - 1); ++yy)
+      for (int xx = max(x - 1, 0); xx <= min(x + 1, g.dims[0] - 1); ++xx) {
+        const int4 cell = g.cells[linear_index(g, xx, yy, zz)];
+        for (uint32_t i = static_cast<uint32_t>(cell.x); i < static_cast<uint32_t>(cell.y); ++i)
+          n += (g.ie_meta[i] & 3u) == kSurface;
+      }
+  cnt[c] = n;
+}
+__global__ void nb_fill_kernel(GridView g, const uint32_t* __restrict__ off, double4* __restrict__ rec) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= g.n_cells) return;
+  const int x = static_cast<int>(c % g.dims[0]), y = static_cast<int>((c / g.dims[0]) % g.dims[1]),
+            z = static_cast<int>(c / (static_cast<uint32_t>(g.dims[0]) * g.dims[1]));
+  uint32_t o = off[c];
+  for (int zz = max(z - 1, 0); zz <= min(z + 1, g.dims[2] - 1); ++zz)
+    for (int yy = max(y - 1, 0); yy <= min(y + 1, g.dims[1] - 1); ++yy)
+      for (int xx = max(x - 1, 0); xx <= min(x + 1, g.dims[0] - 1); ++xx) {
+        const int4 cell = g.cells[linear_index(g, xx, yy, zz)];
+        for (uint32_t i = static_cast<uint32_t>(cell.x); i < static_cast<uint32_t>(cell.y); ++i) {
+          const uint32_t m = g.ie_meta[i];
+          if ((m & 3u) != kSurface) continue;
+          const double4 sc = g.ie_sc[i];
+          const uint64_t w = static_cast<uint64_t>(g.ie_label[i]) | (static_cast<uint64_t>((m >> 2) & 1u) << 32) |
+                             (static_cast<uint64_t>(i) << 33);
+          rec[o++] = make_double4(sc.x, sc.y, sc.z, __longlong_as_double(static_cast<long long>(w)));
+        }
+      }
+}
+
 int rev_order() {
   static const int r = [] {
     const char* e = std::getenv("PCR_REFINE_REV");
@@ -577,6 +664,28 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     gv.ie_rr = rr.get();
     gv.rr_uniform = grid.n_ies && !h;
     gv.rr_radius = r0;
+  }
+  // neighbourhood lists (the reprojection box is a cell's 3x3x3 neighbourhood whenever
+  // 2 * subvoxel_edge spans exactly one voxel each way, i.e. division_factor 2)
+  DBuf<uint32_t> nb_off;
+  DBuf<double4> nb_rec;
+  if (grid.n_cells && grid.n_ies && grid.n_ies < (1ull << 31) && grid.n_cells < (1ull << 31)) {
+    const uint32_t nc = static_cast<uint32_t>(grid.n_cells);
+    DBuf<uint32_t> cnt(nc, s), tot(1, s);
+    nb_off.alloc(nc + 1ull, s);
+    count_launch();
+    nb_count_kernel<<<nb(nc, 256), 256, 0, s>>>(gv, cnt.get());
+    PCR_LAUNCH_CHECK();
+    exclusive_scan_u32(cnt.get(), nb_off.get(), nc, nb_off.get() + nc, s);
+    uint32_t total = 0;
+    d2h(&total, nb_off.get() + nc, 1, s);
+    PCR_CUDA(cudaStreamSynchronize(s));
+    nb_rec.alloc(total ? total : 1, s);
+    count_launch();
+    nb_fill_kernel<<<nb(nc, 256), 256, 0, s>>>(gv, nb_off.get(), nb_rec.get());
+    PCR_LAUNCH_CHECK();
+    gv.nb_off = nb_off.get();
+    gv.nb_rec = nb_rec.get();
   }
   CandIn ci{in.first, step, in.stride, in.tx, in.rx, in.n_inter, in.kind, in.pos, in.label, in.nrm, in.edge, in.coarse_length};
   DBuf<unsigned long long> stats(2, s);
