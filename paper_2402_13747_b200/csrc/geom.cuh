@@ -41,10 +41,12 @@ struct GridView {
   const double4* ie_rr = nullptr;
   double rr_radius = 0.0;
   int rr_uniform = 0;
-  // per cell: the surface IEs of its clamped 3x3x3 neighbourhood in scan order (cells
-  // z->y->x, IEs in cell order) as {sphere centre, label | planar << 32 | ie << 33}
+  // per cell: the surface IEs of its clamped 3x3x3 neighbourhood, scan order (cells
+  // z->y->x, IEs in cell order) stably sorted by label, as
+  // {sphere centre, label | planar << 32 | ie << 33}
   const uint32_t* nb_off = nullptr;  // n_cells + 1
   const double4* nb_rec = nullptr;
+  const uint32_t* nb_lab = nullptr;  // label of each list entry (lists are stably sorted by label)
 };
 
 // Device-resident Scene (scene.hpp:38-46).

@@ -157,13 +157,15 @@ __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, c
     double c_t = 0.0;
     // one flat loop over (cell z→y→x, IE in cell order): lanes of a warp stay in the
     // same loop body whatever their cells' occupancy
-    if (nb) {
-      // the box is the 3x3x3 neighbourhood of the predicted point's cell: one
-      // contiguous list of surface-IE records in the same scan order
-      for (uint32_t j = nb_begin; j < nb_end; ++j) {
+    if (nb && same) {
+      // the box is the 3x3x3 neighbourhood of the predicted point's cell: one list of
+      // its surface-IE records, stably sorted by label, so the same-label candidates
+      // are one contiguous run still in scan order (ties keep the reference's winner)
+      uint32_t j = nb_begin;
+      while (j < nb_end && g.nb_lab[j] < label) ++j;
+      for (; j < nb_end && g.nb_lab[j] == label; ++j) {
         const double4 r4 = g.nb_rec[j];
         const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r4.w));
-        if (same != (static_cast<uint32_t>(w) == label)) continue;
         const uint32_t ie = static_cast<uint32_t>(w >> 33);
         const V3 sc = ld3(r4);
         const double rad = g.rr_uniform ? g.rr_radius : g.ie_sc[ie].w;
@@ -591,7 +593,8 @@ __global__ void nb_count_kernel(GridView g, uint32_t* __restrict__ cnt) {
       }
   cnt[c] = n;
 }
-__global__ void nb_fill_kernel(GridView g, const uint32_t* __restrict__ off, double4* __restrict__ rec) {
+__global__ void nb_fill_kernel(GridView g, const uint32_t* __restrict__ off, double4* __restrict__ rec,
+                               uint32_t* __restrict__ lab) {
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= g.n_cells) return;
   const int x = static_cast<int>(c % g.dims[0]), y = static_cast<int>((c / g.dims[0]) % g.dims[1]),
@@ -607,9 +610,24 @@ __global__ void nb_fill_kernel(GridView g, const uint32_t* __restrict__ off, dou
           const double4 sc = g.ie_sc[i];
           const uint64_t w = static_cast<uint64_t>(g.ie_label[i]) | (static_cast<uint64_t>((m >> 2) & 1u) << 32) |
                              (static_cast<uint64_t>(i) << 33);
-          rec[o++] = make_double4(sc.x, sc.y, sc.z, __longlong_as_double(static_cast<long long>(w)));
+          rec[o] = make_double4(sc.x, sc.y, sc.z, __longlong_as_double(static_cast<long long>(w)));
+          lab[o++] = g.ie_label[i];
         }
       }
+  // stable insertion sort of the list by label (lists are a few dozen entries)
+  const uint32_t b = off[c];
+  for (uint32_t k = b + 1; k < o; ++k) {
+    const uint32_t lk = lab[k];
+    const double4 rk = rec[k];
+    uint32_t m = k;
+    while (m > b && lab[m - 1] > lk) {
+      lab[m] = lab[m - 1];
+      rec[m] = rec[m - 1];
+      --m;
+    }
+    lab[m] = lk;
+    rec[m] = rk;
+  }
 }
 
 int rev_order() {
@@ -667,7 +685,7 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
   }
   // neighbourhood lists (the reprojection box is a cell's 3x3x3 neighbourhood whenever
   // 2 * subvoxel_edge spans exactly one voxel each way, i.e. division_factor 2)
-  DBuf<uint32_t> nb_off;
+  DBuf<uint32_t> nb_off, nb_lab;
   DBuf<double4> nb_rec;
   if (grid.n_cells && grid.n_ies && grid.n_ies < (1ull << 31) && grid.n_cells < (1ull << 31)) {
     const uint32_t nc = static_cast<uint32_t>(grid.n_cells);
@@ -681,11 +699,13 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     d2h(&total, nb_off.get() + nc, 1, s);
     PCR_CUDA(cudaStreamSynchronize(s));
     nb_rec.alloc(total ? total : 1, s);
+    nb_lab.alloc(total ? total : 1, s);
     count_launch();
-    nb_fill_kernel<<<nb(nc, 256), 256, 0, s>>>(gv, nb_off.get(), nb_rec.get());
+    nb_fill_kernel<<<nb(nc, 256), 256, 0, s>>>(gv, nb_off.get(), nb_rec.get(), nb_lab.get());
     PCR_LAUNCH_CHECK();
     gv.nb_off = nb_off.get();
     gv.nb_rec = nb_rec.get();
+    gv.nb_lab = nb_lab.get();
   }
   CandIn ci{in.first, step, in.stride, in.tx, in.rx, in.n_inter, in.kind, in.pos, in.label, in.nrm, in.edge, in.coarse_length};
   DBuf<unsigned long long> stats(2, s);
