@@ -291,6 +291,21 @@ int pcr_run_pipeline_on_scene(pcr_ctx* ctx, const pcr_scene_desc* scene,
 int pcr_run_pipeline_device(pcr_ctx* ctx, const pcr_scene* scene, const pcr_run_config* config,
                             pcr_summary** out);
 
+/* ---- data formats either side of the path --------------------- */
+/* load_point_cloud (io.hpp:15; io.cpp:40-158) straight into a device-resident scene:
+ * ascii or binary_little_endian PLY with float32 x y z nx ny nz and uint32 label,
+ * unknown fixed-size vertex properties skipped. Errors carry the reference's texts
+ * ("cannot open point cloud file: ...", "parse error at line N: ...", "missing field:
+ * x", "truncated vertex data at record R", ...). `rest` supplies edges, radios and
+ * the carrier frequency; its point fields are ignored. */
+int pcr_scene_load_ply(pcr_ctx* ctx, const char* path, const pcr_scene_desc* rest, pcr_scene** out);
+/* The scene's points back on the host (any pointer may be NULL); *n = point count. */
+int pcr_scene_points(pcr_ctx* ctx, const pcr_scene* scene, double* position, double* normal, uint32_t* label,
+                     uint64_t* n);
+/* write_paths (io.hpp:33-34; io.cpp:317-349): the paths JSONL artifact, byte-identical
+ * to the reference's for the same paths and config hash. */
+int pcr_write_paths(pcr_ctx* ctx, const char* path, const pcr_paths* paths, uint64_t config_hash);
+
 /* ---- sharded pipeline: one process per GPU ----------------------------- */
 /* run_pipeline_on_scene split across n_shards contexts (one per GPU). The reference
  * parallelises the same loop over initial hits (tracer.cpp:476-533, parallel_for) and

@@ -114,6 +114,11 @@ def _load(path):
                                                  pp(C.c_double), pp(C.c_double), pp(C.c_uint32)]
         L.pcrref_image_method_paths.argtypes = [pp(C.c_double), C.c_uint32, pp(C.c_double), pp(C.c_double),
                                                 C.c_int, pp(pp(abi.Paths))]
+        L.pcrref_save_point_cloud.argtypes = [C.c_char_p, vp, C.c_int]
+        L.pcrref_load_point_cloud.argtypes = [C.c_char_p, pp(pp(C.c_double)), pp(pp(C.c_double)),
+                                              pp(pp(C.c_uint32)), pp(C.c_uint64)]
+        L.pcrref_free.argtypes = [vp]
+        L.pcrref_write_paths.argtypes = [C.c_char_p, pp(abi.Paths), C.c_uint64]
         _libs[path] = L
     return _libs[path]
 
@@ -308,3 +313,29 @@ def image_method_paths(rect_array, tx, rx, max_order):
         return abi.paths_to_dict(out.contents)
     finally:
         lib().pcrref_free_paths(out)
+
+
+# ---- io.hpp (point clouds, paths artifact) ----------------------------------------------------
+def save_point_cloud(path: str, scene: RefScene, binary: bool = True) -> None:
+    """pcray::save_point_cloud (io.hpp:16-17)."""
+    _check(lib().pcrref_save_point_cloud(path.encode(), scene.handle, int(binary)))
+
+
+def load_point_cloud(path: str) -> dict:
+    """pcray::load_point_cloud (io.hpp:15) -> {position, normal, label}."""
+    pos, nrm, lab, n = C.POINTER(C.c_double)(), C.POINTER(C.c_double)(), C.POINTER(C.c_uint32)(), C.c_uint64()
+    _check(lib().pcrref_load_point_cloud(path.encode(), C.byref(pos), C.byref(nrm), C.byref(lab), C.byref(n)))
+    try:
+        k = n.value
+        return {"position": np.ctypeslib.as_array(pos, (max(k, 1) * 3,))[: 3 * k].reshape(-1, 3).copy(),
+                "normal": np.ctypeslib.as_array(nrm, (max(k, 1) * 3,))[: 3 * k].reshape(-1, 3).copy(),
+                "label": np.ctypeslib.as_array(lab, (max(k, 1),))[:k].copy()}
+    finally:
+        for p in (pos, nrm, lab):
+            lib().pcrref_free(C.cast(p, C.c_void_p))
+
+
+def write_paths(path: str, paths: dict, config_hash: int) -> None:
+    """pcray::write_paths (io.hpp:33-34)."""
+    keep = abi.PathsKeepAlive(paths)
+    _check(lib().pcrref_write_paths(path.encode(), C.byref(keep.paths), config_hash))

@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 
+#include "pcray/io.hpp"
 #include "pcray/oracle.hpp"
 #include "pcray/parallel.hpp"
 #include "pcray/pipeline.hpp"
@@ -684,6 +685,59 @@ int pcrref_image_method_paths(const double* rects, uint32_t n_rect, const double
     pcr_paths* pp = alloc_paths(paths.size(), static_cast<std::uint32_t>(stride));
     for (std::size_t i = 0; i < paths.size(); ++i) put_exact(pp, i, paths[i]);
     *out = pp;
+  });
+}
+
+// save_point_cloud (io.hpp:16-17): the scene's points as a PLY file
+int pcrref_save_point_cloud(const char* path, const void* scene, int binary) {
+  return guarded([&] { save_point_cloud(path, static_cast<const Scene*>(scene)->points, binary != 0); });
+}
+
+// load_point_cloud (io.hpp:15): points into library-allocated arrays (pcrref_free)
+int pcrref_load_point_cloud(const char* path, double** pos, double** nrm, uint32_t** label, uint64_t* n) {
+  return guarded([&] {
+    const auto pts = load_point_cloud(path);
+    *n = pts.size();
+    *pos = alloc<double>(3 * pts.size());
+    *nrm = alloc<double>(3 * pts.size());
+    *label = alloc<uint32_t>(pts.size());
+    for (std::size_t i = 0; i < pts.size(); ++i) {
+      put3(*pos + 3 * i, pts[i].position);
+      put3(*nrm + 3 * i, pts[i].normal);
+      (*label)[i] = pts[i].label;
+    }
+  });
+}
+
+void pcrref_free(void* p) { std::free(p); }
+
+// write_paths (io.hpp:33-34) over exact paths given as a pcr_paths table
+int pcrref_write_paths(const char* path, const pcr_paths* p, uint64_t config_hash) {
+  return guarded([&] {
+    std::vector<ExactPath> v(p->n);
+    for (std::uint64_t i = 0; i < p->n; ++i) {
+      ExactPath& e = v[i];
+      e.tx_id = p->tx_id[i];
+      e.rx_id = p->rx_id[i];
+      e.tx_position = get3(p->tx_position + 3 * i);
+      e.rx_position = get3(p->rx_position + 3 * i);
+      e.total_length = p->length[i];
+      e.delay = p->delay[i];
+      e.converged = p->converged[i] != 0;
+      e.gradient_norm = p->gradient_norm[i];
+      for (std::uint32_t k = 0; k < p->n_inter[i]; ++k) {
+        const std::size_t j = i * p->stride + k;
+        Interaction it;
+        it.kind = static_cast<InteractionKind>(p->kind[j]);
+        it.position = get3(p->position + 3 * j);
+        it.label = p->label[j];
+        it.normal = get3(p->normal + 3 * j);
+        it.ie_index = p->ie_index[j];
+        it.edge_index = p->edge_index[j];
+        e.interactions.push_back(it);
+      }
+    }
+    write_paths(path, v, config_hash);
   });
 }
 

@@ -347,6 +347,36 @@ int pcr_run_pipeline_device(pcr_ctx* ctx, const pcr_scene* scene, const pcr_run_
   });
 }
 
+int pcr_scene_load_ply(pcr_ctx* ctx, const char* path, const pcr_scene_desc* rest, pcr_scene** out) {
+  return guarded(ctx, [&] {
+    if (!path || !rest || !out) throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    auto* sc = new pcr_scene();
+    try {
+      pcr::api_scene_load_ply(ctx->c, path, *rest, sc->s);
+    } catch (...) {
+      delete sc;
+      throw;
+    }
+    *out = sc;
+  });
+}
+
+int pcr_scene_points(pcr_ctx* ctx, const pcr_scene* scene, double* position, double* normal, uint32_t* label,
+                     uint64_t* n) {
+  return guarded(ctx, [&] {
+    if (!scene) throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    if (n) *n = scene->s.n_points;
+    pcr::api_scene_points(ctx->c, scene->s, position, normal, label);
+  });
+}
+
+int pcr_write_paths(pcr_ctx* ctx, const char* path, const pcr_paths* paths, uint64_t config_hash) {
+  return guarded(ctx, [&] {
+    if (!path || !paths) throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    pcr::api_write_paths(path, *paths, config_hash);
+  });
+}
+
 int pcr_shard_trace(pcr_ctx* ctx, const pcr_scene* scene, const pcr_run_config* config, uint32_t shard,
                     uint32_t n_shards, uint64_t* n_rows, uint64_t* row_bytes) {
   return guarded(ctx, [&] {

@@ -52,6 +52,7 @@ struct GridDev {
   int dv = 2;
   double sub_edge = 0, sub_radius = 0, voxel_radius = 0, hit_eps = 0;
   uint64_t n_cells = 0, n_ies = 0, n_pidx = 0;
+  bool march_ok = false;  // cells[].z holds compute_march_distances' values (set by it)
   DBuf<int4> cells;
   DBuf<uint32_t> meta, label, edge, rx, voxel, sub, pidx;
   DBuf<double4> sc, rp, pp, pn, seg_s, seg_e;
@@ -96,6 +97,7 @@ struct GridDev {
     v.ie_edge = edge.get();
     v.ie_rx = rx.get();
     v.point_indices = pidx.get();
+    v.march_ok = march_ok ? 1 : 0;
     return v;
   }
   void alloc_ies(uint64_t n, cudaStream_t s) {

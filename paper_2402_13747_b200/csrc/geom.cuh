@@ -36,6 +36,7 @@ struct GridView {
   const uint32_t* ie_edge;
   const uint32_t* ie_rx;
   const uint32_t* point_indices;
+  int march_ok = 0;  // cells[].z are exact march distances (visibility may skip empty space)
   // refinement scan records (built per refine call): {sphere centre, label | meta << 32};
   // rr_radius is every IE's sphere radius when rr_uniform (as build_grid makes them)
   const double4* ie_rr = nullptr;
@@ -405,7 +406,25 @@ __device__ inline bool segment_visible(const V3& origin, const V3& target, uint3
   Walker w;
   w.init(g, origin, d, 0.0, dist);
   int axis = -1;  // -1: full 27-neighbourhood
+  int skip = 0;
   while (w.active) {
+    // empty-space skipping (exact): march(v) = m >= 2 means every cell within
+    // Chebyshev distance m-1 of v is empty, so N(u) is empty for v and for the next
+    // m-2 voxels of the walk (each step moves to an adjacent voxel); the walk itself
+    // is unchanged, only the screening of empty neighbourhoods is left out. The next
+    // screened voxel's far slab still covers its neighbourhood: the rest of it lies
+    // in N(previous voxel), screened or empty.
+    if (skip > 0) {
+      --skip;
+      axis = w.advance(g);
+      continue;
+    }
+    const int m = g.march_ok ? g.cells[linear_index(g, w.v[0], w.v[1], w.v[2])].z : 0;
+    if (m >= 2) {
+      skip = m - 2;
+      axis = w.advance(g);
+      continue;
+    }
     const int sa = axis;
     const int lo0 = (sa == 0) ? w.step[0] : -1, hi0 = (sa == 0) ? w.step[0] : 1;
     const int lo1 = (sa == 1) ? w.step[1] : -1, hi1 = (sa == 1) ? w.step[1] : 1;
@@ -460,7 +479,20 @@ __device__ inline bool warp_segment_visible(const V3& origin, const V3& target, 
   Walker w;
   w.init(g, origin, d, 0.0, dist);
   int axis = -1;
+  int skip = 0;
   while (w.active) {
+    // empty-space skipping, as in segment_visible (warp-uniform)
+    if (skip > 0) {
+      --skip;
+      axis = w.advance(g);
+      continue;
+    }
+    const int m = g.march_ok ? g.cells[linear_index(g, w.v[0], w.v[1], w.v[2])].z : 0;
+    if (m >= 2) {
+      skip = m - 2;
+      axis = w.advance(g);
+      continue;
+    }
     int off[3];
     bool mine;
     if (axis < 0) {

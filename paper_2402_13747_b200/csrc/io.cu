@@ -1,0 +1,312 @@
+// io.cu — the data formats either side of the hot path:
+//
+// * point-cloud ingest (load_point_cloud, proj/src/io.cpp:40-158) straight into the
+//   device-resident Scene: the header is parsed on the host with the reference's
+//   rules and error texts; binary_little_endian vertex data is streamed in chunks
+//   through two pinned buffers (read chunk k+1 while chunk k is copied and decoded)
+//   and a decode kernel picks x, y, z, nx, ny, nz (float32 -> FP64, exact) and label
+//   out of each row at the header's property offsets, skipping unknown properties;
+//   ascii data is parsed on the host as the reference does (istream >> double).
+// * the paths JSONL writer (write_paths, proj/src/io.cpp:317-349): same header line,
+//   same field order, %.9g numbers, records in the order given.
+#include <cuda_runtime.h>
+
+#include <cerrno>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "host_alloc.hpp"
+#include "pipeline.hpp"
+
+namespace pcr {
+
+namespace {
+
+[[noreturn]] void header_error(int line_no, const std::string& what) {
+  throw Error(PCR_ERR_RUNTIME, "parse error at line " + std::to_string(line_no) + ": " + what);
+}
+
+size_t ply_type_size(const std::string& type, int line_no) {
+  if (type == "char" || type == "int8" || type == "uchar" || type == "uint8") return 1;
+  if (type == "short" || type == "int16" || type == "ushort" || type == "uint16") return 2;
+  if (type == "int" || type == "int32" || type == "uint" || type == "uint32" || type == "float" ||
+      type == "float32")
+    return 4;
+  if (type == "double" || type == "float64") return 8;
+  header_error(line_no, "unknown property type '" + type + "'");
+}
+
+struct PlyProp {
+  std::string type, name;
+  size_t offset = 0;
+};
+
+struct PlyHeader {
+  bool binary = false;
+  size_t vertex_count = 0, stride = 0;
+  std::vector<PlyProp> props;
+  int idx[7];  // x y z nx ny nz label
+};
+
+// Header rules of load_point_cloud (io.cpp:40-122), same messages.
+PlyHeader parse_header(std::istream& in) {
+  PlyHeader h;
+  int line_no = 0;
+  auto next_line = [&](std::string& line) {
+    if (!std::getline(in, line)) header_error(line_no + 1, "unexpected end of header");
+    ++line_no;
+    if (!line.empty() && line.back() == '\r') line.pop_back();
+  };
+  std::string line;
+  next_line(line);
+  if (line != "ply") header_error(line_no, "expected 'ply' magic");
+  next_line(line);
+  if (line == "format ascii 1.0")
+    h.binary = false;
+  else if (line == "format binary_little_endian 1.0")
+    h.binary = true;
+  else
+    header_error(line_no, "unsupported format '" + line + "'");
+  bool in_vertex = false, vertex_seen = false;
+  for (;;) {
+    next_line(line);
+    std::istringstream iss(line);
+    std::string word;
+    iss >> word;
+    if (word == "comment" || word == "obj_info" || word.empty()) continue;
+    if (word == "end_header") break;
+    if (word == "element") {
+      std::string name;
+      long long count = -1;
+      if (!(iss >> name >> count) || count < 0) header_error(line_no, "malformed element declaration");
+      if (name == "vertex") {
+        if (vertex_seen) header_error(line_no, "duplicate vertex element");
+        vertex_seen = true;
+        in_vertex = true;
+        h.vertex_count = static_cast<size_t>(count);
+      } else {
+        if (!vertex_seen && count > 0) header_error(line_no, "element '" + name + "' precedes vertex data");
+        in_vertex = false;
+      }
+      continue;
+    }
+    if (word == "property") {
+      if (!in_vertex) continue;
+      PlyProp p;
+      iss >> p.type;
+      if (p.type == "list") header_error(line_no, "list property in vertex element");
+      iss >> p.name;
+      if (p.name.empty()) header_error(line_no, "malformed property declaration");
+      p.offset = h.stride;
+      h.stride += ply_type_size(p.type, line_no);
+      h.props.push_back(p);
+      continue;
+    }
+    header_error(line_no, "unknown header keyword '" + word + "'");
+  }
+  if (!vertex_seen) header_error(line_no, "no vertex element");
+  const char* required[] = {"x", "y", "z", "nx", "ny", "nz", "label"};
+  for (int r = 0; r < 7; ++r) {
+    h.idx[r] = -1;
+    for (size_t i = 0; i < h.props.size(); ++i)
+      if (h.props[i].name == required[r]) h.idx[r] = static_cast<int>(i);  // last declaration wins
+    if (h.idx[r] < 0) throw Error(PCR_ERR_RUNTIME, std::string("missing field: ") + required[r]);
+    const std::string& t = h.props[h.idx[r]].type;
+    if (r < 6 && t != "float" && t != "float32")
+      throw Error(PCR_ERR_RUNTIME, std::string("field ") + required[r] + " must be float32");
+    if (r == 6 && t != "uint" && t != "uint32") throw Error(PCR_ERR_RUNTIME, "field label must be uint32");
+  }
+  return h;
+}
+
+struct RowLayout {
+  uint32_t stride;
+  uint32_t off[7];
+};
+
+// One thread per vertex row: float32 fields widened to FP64 (exact), label as is.
+__global__ void ply_decode_kernel(const uint8_t* __restrict__ rows, uint64_t n, RowLayout L, uint64_t first,
+                                  double* __restrict__ pos, double* __restrict__ nrm, uint32_t* __restrict__ label) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint8_t* r = rows + i * L.stride;
+  float f[6];
+  for (int k = 0; k < 6; ++k) memcpy(&f[k], r + L.off[k], 4);
+  uint32_t lab;
+  memcpy(&lab, r + L.off[6], 4);
+  const uint64_t v = first + i;
+  pos[3 * v] = f[0];
+  pos[3 * v + 1] = f[1];
+  pos[3 * v + 2] = f[2];
+  nrm[3 * v] = f[3];
+  nrm[3 * v + 1] = f[4];
+  nrm[3 * v + 2] = f[5];
+  label[v] = lab;
+}
+
+struct Pinned {
+  uint8_t* p = nullptr;
+  explicit Pinned(size_t n) {
+    if (cudaMallocHost(&p, n ? n : 1) != cudaSuccess) throw Error(PCR_ERR_NOMEM, "cudaMallocHost failed");
+  }
+  ~Pinned() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+// The non-point parts of the scene (edges, radios, frequency) as upload_scene does.
+void upload_rest(Ctx& ctx, const pcr_scene_desc& d, SceneDev& S) {
+  cudaStream_t s = ctx.stream;
+  S.n_edges = d.n_edges;
+  S.h_edges.assign(d.edge_geometry, d.edge_geometry + 12ull * d.n_edges);
+  S.h_edge_label.assign(d.edge_label, d.edge_label + d.n_edges);
+  S.edges.alloc(12ull * d.n_edges + 12, s);
+  S.edge_label.alloc(d.n_edges + 1ull, s);
+  h2d(S.edges.get(), S.h_edges.data(), S.h_edges.size(), s);
+  h2d(S.edge_label.get(), S.h_edge_label.data(), S.h_edge_label.size(), s);
+  S.h_tx.assign(d.tx_position, d.tx_position + 3ull * d.n_tx);
+  S.h_tx_id.assign(d.tx_id, d.tx_id + d.n_tx);
+  S.h_rx.assign(d.rx_position, d.rx_position + 3ull * d.n_rx);
+  S.h_rx_id.assign(d.rx_id, d.rx_id + d.n_rx);
+  S.rx_pos.alloc(3ull * d.n_rx + 3, s);
+  S.rx_id.alloc(d.n_rx + 1ull, s);
+  h2d(S.rx_pos.get(), S.h_rx.data(), S.h_rx.size(), s);
+  h2d(S.rx_id.get(), S.h_rx_id.data(), S.h_rx_id.size(), s);
+  S.carrier_frequency_hz = d.carrier_frequency_hz;
+}
+
+std::string fmt9(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof(buf), "%.9g", v);
+  return buf;
+}
+
+}  // namespace
+
+void api_scene_load_ply(Ctx& ctx, const char* path, const pcr_scene_desc& rest, SceneDev& S) {
+  cudaStream_t s = ctx.stream;
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw Error(PCR_ERR_RUNTIME, std::string("cannot open point cloud file: ") + path);
+  const PlyHeader h = parse_header(in);
+  const size_t n = h.vertex_count;
+  S.n_points = n;
+  S.pos.alloc(3 * n + 3, s);
+  S.nrm.alloc(3 * n + 3, s);
+  S.label.alloc(n + 1, s);
+  if (h.binary) {
+    RowLayout L;
+    L.stride = static_cast<uint32_t>(h.stride);
+    for (int r = 0; r < 7; ++r) L.off[r] = static_cast<uint32_t>(h.props[h.idx[r]].offset);
+    // chunks of whole rows, double-buffered: the file read of chunk k+1 overlaps the
+    // copy + decode of chunk k
+    const size_t rows_per_chunk = std::max<size_t>(1, (size_t(64) << 20) / std::max<size_t>(1, h.stride));
+    const size_t chunk_bytes = rows_per_chunk * h.stride;
+    Pinned host[2] = {Pinned(chunk_bytes), Pinned(chunk_bytes)};
+    DBuf<uint8_t> dev[2];
+    dev[0].alloc(chunk_bytes, s);
+    dev[1].alloc(chunk_bytes, s);
+    cudaEvent_t done[2];
+    PCR_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+    PCR_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+    bool pending[2] = {false, false};
+    size_t v = 0;
+    int b = 0;
+    try {
+      while (v < n) {
+        const size_t rows = std::min(rows_per_chunk, n - v);
+        if (pending[b]) PCR_CUDA(cudaEventSynchronize(done[b]));  // buffer b is free again
+        in.read(reinterpret_cast<char*>(host[b].p), static_cast<std::streamsize>(rows * h.stride));
+        const size_t got = static_cast<size_t>(in.gcount());
+        if (got < rows * h.stride)
+          throw Error(PCR_ERR_RUNTIME, "truncated vertex data at record " + std::to_string(v + got / h.stride));
+        PCR_CUDA(cudaMemcpyAsync(dev[b].get(), host[b].p, rows * h.stride, cudaMemcpyHostToDevice, s));
+        g_h2d_bytes += rows * h.stride;
+        count_launch();
+        ply_decode_kernel<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(
+            dev[b].get(), rows, L, v, S.pos.get(), S.nrm.get(), S.label.get());
+        PCR_LAUNCH_CHECK();
+        PCR_CUDA(cudaEventRecord(done[b], s));
+        pending[b] = true;
+        v += rows;
+        b ^= 1;
+      }
+      PCR_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      cudaStreamSynchronize(s);
+      cudaEventDestroy(done[0]);
+      cudaEventDestroy(done[1]);
+      throw;
+    }
+    cudaEventDestroy(done[0]);
+    cudaEventDestroy(done[1]);
+  } else {
+    // ascii: every property parsed as a double in declaration order (io.cpp:139-155)
+    std::vector<double> pos(3 * n), nrm(3 * n), values(h.props.size());
+    std::vector<uint32_t> lab(n);
+    std::string line;
+    for (size_t v = 0; v < n; ++v) {
+      if (!std::getline(in, line)) throw Error(PCR_ERR_RUNTIME, "truncated vertex data at record " + std::to_string(v));
+      std::istringstream iss(line);
+      for (size_t i = 0; i < h.props.size(); ++i)
+        if (!(iss >> values[i])) throw Error(PCR_ERR_RUNTIME, "malformed vertex data at record " + std::to_string(v));
+      for (int a = 0; a < 3; ++a) {
+        pos[3 * v + a] = values[h.idx[a]];
+        nrm[3 * v + a] = values[h.idx[3 + a]];
+      }
+      lab[v] = static_cast<uint32_t>(values[h.idx[6]]);
+    }
+    h2d(S.pos.get(), pos.data(), pos.size(), s);
+    h2d(S.nrm.get(), nrm.data(), nrm.size(), s);
+    h2d(S.label.get(), lab.data(), lab.size(), s);
+  }
+  upload_rest(ctx, rest, S);
+  PCR_CUDA(cudaStreamSynchronize(s));
+}
+
+void api_scene_points(Ctx& ctx, const SceneDev& S, double* pos, double* nrm, uint32_t* label) {
+  cudaStream_t s = ctx.stream;
+  if (pos) d2h(pos, S.pos.get(), 3 * S.n_points, s);
+  if (nrm) d2h(nrm, S.nrm.get(), 3 * S.n_points, s);
+  if (label) d2h(label, S.label.get(), S.n_points, s);
+  PCR_CUDA(cudaStreamSynchronize(s));
+}
+
+// write_paths (io.cpp:317-349): header with the config hash, then one record per path.
+void api_write_paths(const char* path, const pcr_paths& p, uint64_t config_hash) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw Error(PCR_ERR_RUNTIME, std::string("cannot write paths file: ") + path);
+  char hex[17];
+  std::snprintf(hex, sizeof(hex), "%016llx", static_cast<unsigned long long>(config_hash));
+  std::string buf;
+  buf.reserve(1 << 20);
+  buf += "{\"artifact\":\"paths\",\"version\":1,\"config_hash\":\"";
+  buf += hex;
+  buf += "\"}\n";
+  for (uint64_t i = 0; i < p.n; ++i) {
+    buf += "{\"tx_id\":" + std::to_string(p.tx_id[i]) + ",\"rx_id\":" + std::to_string(p.rx_id[i]) +
+           ",\"delay_s\":" + fmt9(p.delay[i]) + ",\"length_m\":" + fmt9(p.length[i]) +
+           ",\"converged\":" + (p.converged[i] ? "true" : "false") + ",\"gradient_norm\":" +
+           fmt9(p.gradient_norm[i]) + ",\"interactions\":[";
+    for (uint32_t k = 0; k < p.n_inter[i]; ++k) {
+      const size_t j = i * p.stride + k;
+      if (k) buf += ",";
+      buf += std::string("{\"kind\":\"") + (p.kind[j] == 0 ? "reflection" : "diffraction") + "\",\"position\":[" +
+             fmt9(p.position[3 * j]) + "," + fmt9(p.position[3 * j + 1]) + "," + fmt9(p.position[3 * j + 2]) +
+             "],\"label\":" + std::to_string(p.label[j]) + "}";
+    }
+    buf += "]}\n";
+    if (buf.size() > (1u << 20)) {
+      out.write(buf.data(), static_cast<std::streamsize>(buf.size()));
+      buf.clear();
+    }
+  }
+  out.write(buf.data(), static_cast<std::streamsize>(buf.size()));
+  if (!out) throw Error(PCR_ERR_RUNTIME, std::string("write failure: ") + path);
+}
+
+}  // namespace pcr

@@ -21,6 +21,10 @@ void api_refine_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, cons
 // pipeline (pipeline.cu)
 void api_run_pipeline_on_scene(Ctx& ctx, const pcr_scene_desc& desc, const pcr_run_config& cfg, pcr_summary** out);
 void api_run_pipeline_device(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, pcr_summary** out);
+// data formats (io.cu)
+void api_scene_load_ply(Ctx& ctx, const char* path, const pcr_scene_desc& rest, SceneDev& S);
+void api_scene_points(Ctx& ctx, const SceneDev& S, double* pos, double* nrm, uint32_t* label);
+void api_write_paths(const char* path, const pcr_paths& p, uint64_t config_hash);
 // sharded pipeline (pipeline.cu)
 void api_shard_trace(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, uint32_t shard, uint32_t n_shards,
                      uint64_t* n_rows, uint64_t* row_bytes);

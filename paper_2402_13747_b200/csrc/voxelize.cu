@@ -584,6 +584,7 @@ void compute_march_distances_device(Ctx& ctx, GridDev& grid) {
     count_launch();
     fill_march_kernel<<<blocks_for(n, kThreads), kThreads, 0, s>>>(grid.cells.get(), n, kMarchNoIes);
     PCR_LAUNCH_CHECK();
+    grid.march_ok = true;
     return;
   }
   const int dx = grid.dims[0], dy = grid.dims[1], dz = grid.dims[2];
@@ -598,6 +599,7 @@ void compute_march_distances_device(Ctx& ctx, GridDev& grid) {
   count_launch();
   dt_axis_kernel<<<blocks_for(n, kThreads), kThreads, 0, s>>>(g2.get(), nullptr, dx, dy, dz, 2, grid.cells.get());
   PCR_LAUNCH_CHECK();
+  grid.march_ok = true;
 }
 
 void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int division_factor,

@@ -63,6 +63,9 @@ def lib():
         L.pcr_refine_batch.argtypes = [vp, vp, vp, pp(abi.Paths), pp(abi.RefineParams), pp(pp(abi.Outcomes))]
         L.pcr_run_pipeline_on_scene.argtypes = [vp, pp(abi.SceneDesc), pp(abi.RunConfig), pp(pp(abi.Summary))]
         L.pcr_run_pipeline_device.argtypes = [vp, vp, pp(abi.RunConfig), pp(pp(abi.Summary))]
+        L.pcr_scene_load_ply.argtypes = [vp, C.c_char_p, pp(abi.SceneDesc), pp(vp)]
+        L.pcr_scene_points.argtypes = [vp, vp, pp(C.c_double), pp(C.c_double), pp(C.c_uint32), pp(C.c_uint64)]
+        L.pcr_write_paths.argtypes = [vp, C.c_char_p, pp(abi.Paths), C.c_uint64]
         L.pcr_shard_trace.argtypes = [vp, vp, pp(abi.RunConfig), C.c_uint32, C.c_uint32, pp(C.c_uint64),
                                       pp(C.c_uint64)]
         L.pcr_shard_rows.argtypes = [vp, vp]
@@ -96,7 +99,8 @@ EXPORTED_SYMBOLS = [
     "pcr_segment_visible_batch", "pcr_refine_batch", "pcr_run_pipeline_on_scene", "pcr_config_hash",
     "pcr_run_config_defaults", "pcr_free_paths", "pcr_free_initial_hits", "pcr_free_outcomes",
     "pcr_free_summary", "pcr_free_receptions", "pcr_run_pipeline_device", "pcr_shard_trace", "pcr_shard_rows",
-    "pcr_shard_refine", "pcr_shard_outcomes", "pcr_shard_stats_get", "pcr_shard_finish",
+    "pcr_shard_refine", "pcr_shard_outcomes", "pcr_shard_stats_get", "pcr_shard_finish", "pcr_scene_load_ply",
+    "pcr_scene_points", "pcr_write_paths",
 ]
 
 
@@ -143,6 +147,40 @@ class DeviceScene:
         h = C.c_void_p()
         self.ctx.check(lib().pcr_scene_upload(self.ctx.handle, C.byref(self.keep.desc), C.byref(h)))
         self.handle = h
+
+    @classmethod
+    def from_ply(cls, path: str, rest: Scene | None = None, ctx: Context | None = None,
+                 host_mirror: bool = True) -> "DeviceScene":
+        """pcray::load_point_cloud (io.hpp:15) straight into HBM (pcr_scene_load_ply); `rest`
+        supplies edges, radios and the carrier frequency (its points are ignored).
+        host_mirror=False skips reading the points back into `.scene`."""
+        self = cls.__new__(cls)
+        self.ctx = ctx or Context.default()
+        self.keep = abi.SceneKeepAlive(rest or Scene())
+        h = C.c_void_p()
+        self.ctx.check(lib().pcr_scene_load_ply(self.ctx.handle, os.fsencode(path), C.byref(self.keep.desc),
+                                                C.byref(h)))
+        self.handle = h
+        r = self.keep.scene
+        if not host_mirror:
+            self.scene = r
+            return self
+        pts = self.points()
+        self.scene = Scene(pts["position"], pts["normal"], pts["label"], r.edges, r.edge_label, r.tx, r.tx_id,
+                           r.rx, r.rx_id, r.carrier_frequency_hz)
+        return self
+
+    def points(self) -> dict:
+        """The resident points back on the host (pcr_scene_points)."""
+        n = C.c_uint64()
+        self.ctx.check(lib().pcr_scene_points(self.ctx.handle, self.handle, None, None, None, C.byref(n)))
+        k = n.value
+        pos, nrm, lab = np.zeros((k, 3)), np.zeros((k, 3)), np.zeros(k, np.uint32)
+        dp = C.POINTER(C.c_double)
+        self.ctx.check(lib().pcr_scene_points(self.ctx.handle, self.handle, pos.ctypes.data_as(dp),
+                                              nrm.ctypes.data_as(dp), lab.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                              C.byref(n)))
+        return {"position": pos, "normal": nrm, "label": lab}
 
     def __del__(self):
         if getattr(self, "handle", None) and _lib is not None:
@@ -302,6 +340,18 @@ def run_pipeline_device(scene: DeviceScene, config: RunConfig | None = None) -> 
         return abi.summary_to_dict(out.contents)
     finally:
         lib().pcr_free_summary(out)
+
+
+def load_point_cloud(path: str, rest: Scene | None = None, ctx: Context | None = None) -> DeviceScene:
+    """pcray::load_point_cloud (io.hpp:15), device-resident result."""
+    return DeviceScene.from_ply(path, rest, ctx)
+
+
+def write_paths(path: str, paths: dict, config_hash: int, ctx: Context | None = None) -> None:
+    """pcray::write_paths (io.hpp:33-34): the paths JSONL artifact."""
+    ctx = ctx or Context.default()
+    keep = abi.PathsKeepAlive(paths)
+    ctx.check(lib().pcr_write_paths(ctx.handle, os.fsencode(path), C.byref(keep.paths), config_hash))
 
 
 # ---- sharded pipeline (one process per GPU; orchestration in shard.py) ---------------------------
