@@ -26,7 +26,17 @@ struct Error : std::runtime_error {
     }                                                                                           \
   } while (0)
 
-#define PCR_LAUNCH_CHECK() PCR_CUDA(cudaGetLastError())
+// Launch errors; with PCR_SYNC_LAUNCHES=1 in the environment every checked launch is
+// also synchronised, so an asynchronous fault names the kernel's source line (debug aid).
+bool sync_launches();
+inline void launch_check(const char* file, int line) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && sync_launches()) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess)
+    throw Error(e == cudaErrorMemoryAllocation ? 3 : 2,
+                std::string("cuda launch at ") + file + ":" + std::to_string(line) + ": " + cudaGetErrorString(e));
+}
+#define PCR_LAUNCH_CHECK() ::pcr::launch_check(__FILE__, __LINE__)
 
 // Stream-ordered device buffer (cudaMallocAsync pool); never copied, only moved.
 template <typename T>

@@ -1,8 +1,8 @@
 // pipeline.cu — run_pipeline_on_scene (proj/src/pipeline.cpp:99-212) over the
-// device stages, plus the host-side pieces of the reference contract that sit
-// outside the hot path: validate_scene (scene.cpp:31-91), dedup_by_label /
-// dedup_by_fresnel (refine.cpp:288-372), the final output order
-// (pipeline.cpp:194-207) and config_hash (pipeline.cpp:89-97).
+// device stages: validate_scene (scene.cpp:31-91) on the device, the stage calls,
+// dedup_by_label / dedup_by_fresnel (refine.cpp:288-372) and the final output order
+// (pipeline.cpp:194-207) on the device, config_hash (pipeline.cpp:89-97); plus the
+// sharded variant of the same run.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -18,6 +18,7 @@
 #include "host_alloc.hpp"
 #include "pipeline.hpp"
 #include "shard_rows.cuh"
+#include "sort.cuh"
 #include "stages.cuh"
 #include "trace.cuh"
 
@@ -147,102 +148,6 @@ struct EP {
   double total_length, delay, gnorm;
   bool converged;
 };
-
-bool lex_less(const V3& a, const V3& b) {
-  if (a.x != b.x) return a.x < b.x;
-  if (a.y != b.y) return a.y < b.y;
-  return a.z < b.z;
-}
-bool positions_lex_less(const EP& a, const EP& b) {
-  for (size_t k = 0; k < std::min(a.its.size(), b.its.size()); ++k)
-    if (a.its[k].pos != b.its[k].pos) return lex_less(a.its[k].pos, b.its[k].pos);
-  return a.its.size() < b.its.size();
-}
-void sort_by_delay(std::vector<EP>& v) {
-  std::sort(v.begin(), v.end(), [](const EP& a, const EP& b) {
-    if (a.delay != b.delay) return a.delay < b.delay;
-    if (a.tx_id != b.tx_id) return a.tx_id < b.tx_id;
-    if (a.rx_id != b.rx_id) return a.rx_id < b.rx_id;
-    return positions_lex_less(a, b);
-  });
-}
-std::vector<int> kinds(const EP& p) {
-  std::vector<int> k;
-  for (const It& i : p.its) k.push_back(i.kind);
-  return k;
-}
-std::vector<uint32_t> labels_of(const EP& p) {
-  std::vector<uint32_t> k;
-  for (const It& i : p.its) k.push_back(i.label);
-  return k;
-}
-
-// dedup_by_label (refine.cpp:324-343)
-std::vector<EP> dedup_by_label(std::vector<EP> paths) {
-  using Key = std::tuple<uint32_t, uint32_t, std::vector<int>, std::vector<uint32_t>>;
-  std::map<Key, size_t> best;
-  for (size_t i = 0; i < paths.size(); ++i) {
-    Key key{paths[i].tx_id, paths[i].rx_id, kinds(paths[i]), labels_of(paths[i])};
-    auto [it, inserted] = best.try_emplace(std::move(key), i);
-    if (inserted) continue;
-    const EP& cur = paths[it->second];
-    const EP& cand = paths[i];
-    if (cand.total_length < cur.total_length ||
-        (cand.total_length == cur.total_length && positions_lex_less(cand, cur)))
-      it->second = i;
-  }
-  std::vector<EP> out;
-  out.reserve(best.size());
-  for (const auto& kv : best) out.push_back(paths[kv.second]);
-  sort_by_delay(out);
-  return out;
-}
-
-// dedup_by_fresnel (refine.cpp:345-372)
-// Kept paths are bucketed by (tx, rx, kind sequence): a path is only ever compared
-// with kept paths of its own bucket, visited in kept (= delay) order, which is the
-// reference's scan with the non-matching entries skipped.
-std::vector<EP> dedup_by_fresnel(std::vector<EP> paths, double freq) {
-  const double lambda = kC / freq;
-  sort_by_delay(paths);
-  std::vector<EP> kept;
-  std::map<std::tuple<uint32_t, uint32_t, std::vector<int>>, std::vector<size_t>> buckets;
-  for (EP& p : paths) {
-    bool dup = false;
-    auto& bucket = buckets[{p.tx_id, p.rx_id, kinds(p)}];
-    for (size_t qi : bucket) {
-      const EP& q = kept[qi];
-      bool inside = true;
-      for (size_t k = 0; k < p.its.size() && inside; ++k) {
-        const V3 a = k == 0 ? q.tx : q.its[k - 1].pos;
-        const V3 b = q.its[k].pos;
-        const V3& pt = p.its[k].pos;
-        inside = norm(pt - a) + norm(pt - b) <= norm(b - a) + 0.5 * lambda;
-      }
-      if (inside) {
-        dup = true;
-        break;
-      }
-    }
-    if (!dup) {
-      bucket.push_back(kept.size());
-      kept.push_back(std::move(p));
-    }
-  }
-  return kept;
-}
-
-void final_sort(std::vector<EP>& v) {
-  std::sort(v.begin(), v.end(), [](const EP& a, const EP& b) {
-    if (a.tx_id != b.tx_id) return a.tx_id < b.tx_id;
-    if (a.rx_id != b.rx_id) return a.rx_id < b.rx_id;
-    if (a.delay != b.delay) return a.delay < b.delay;
-    if (a.its.size() != b.its.size()) return a.its.size() < b.its.size();
-    for (size_t k = 0; k < a.its.size(); ++k)
-      if (a.its[k].pos != b.its[k].pos) return lex_less(a.its[k].pos, b.its[k].pos);
-    return false;
-  });
-}
 
 // ---- combined candidate set on the device -----------------------------------------------------
 struct CandSet {
@@ -547,65 +452,458 @@ void refine_cands(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const Ca
   refine_device(ctx, grid, scene, in, rp, ro);
 }
 
-// Refinement outcomes -> ExactPaths (pipeline.cpp:148-187), counting rejects and
-// iterations; LOS candidates pass through.
-std::vector<EP> collect_paths(Ctx& ctx, const CandSet& cs, const RefineDevOut& ro, pcr_summary* S) {
-  cudaStream_t s = ctx.stream;
-  const uint32_t stride = cs.stride;
-  const size_t n = cs.n, ms = n * stride;
-  std::vector<uint8_t> has(n), kind(ms);
-  std::vector<int32_t> reason(n);
-  std::vector<uint32_t> txid(n), rxid(n), ni(n), lab(ms), ie(ms), ed(ms), iters(n);
-  std::vector<double> txp(3 * n), rxp(3 * n), pos(3 * ms), nrm(3 * ms), len(n), del(n), gn(n);
-  d2h(has.data(), ro.has_path.get(), n, s);
-  d2h(reason.data(), ro.reason.get(), n, s);
-  d2h(iters.data(), ro.iters.get(), n, s);
-  d2h(txid.data(), cs.tx_id.get(), n, s);
-  d2h(rxid.data(), cs.rx_id.get(), n, s);
-  d2h(ni.data(), cs.n_inter.get(), n, s);
-  d2h(kind.data(), cs.kind.get(), ms, s);
-  d2h(ie.data(), cs.ie.get(), ms, s);
-  d2h(ed.data(), cs.edge.get(), ms, s);
-  d2h(txp.data(), cs.tx_pos.get(), 3 * n, s);
-  d2h(rxp.data(), cs.rx_pos.get(), 3 * n, s);
-  d2h(pos.data(), ro.pos.get(), 3 * ms, s);
-  d2h(nrm.data(), ro.nrm.get(), 3 * ms, s);
-  d2h(lab.data(), ro.label.get(), ms, s);
-  d2h(len.data(), ro.length.get(), n, s);
-  d2h(del.data(), ro.delay.get(), n, s);
-  d2h(gn.data(), ro.gnorm.get(), n, s);
-  PCR_CUDA(cudaStreamSynchronize(s));
-  std::vector<EP> exact;
-  for (size_t i = 0; i < n; ++i) {
-    S->refine_iterations += iters[i];
-    if (!has[i]) {
-      ++S->rejected[reason[i] & 3];
-      continue;
-    }
-    EP e;
-    e.tx_id = txid[i];
-    e.rx_id = rxid[i];
-    e.tx = load3(&txp[3 * i]);
-    e.rx = load3(&rxp[3 * i]);
-    e.total_length = len[i];
-    e.delay = del[i];
-    e.gnorm = gn[i];
-    e.converged = true;
-    for (uint32_t q = 0; q < ni[i]; ++q) {
-      const size_t j = i * stride + q;
-      e.its.push_back(It{kind[j], load3(&pos[3 * j]), load3(&nrm[3 * j]), lab[j], ie[j], ed[j]});
-    }
-    exact.push_back(std::move(e));
-  }
-  S->refined_paths = exact.size();
-  return exact;
+// ---- dedup + final order on the device --------------------------------------
+// dedup_by_label (refine.cpp:324-343), dedup_by_fresnel (:345-372) and the final order
+// (pipeline.cpp:194-207) over the refinement outcomes in HBM; only the surviving paths
+// come back to the host. Orders are stable LSD radix sorts on (delay, tx, rx) keys; the
+// comparators' last fields (size, positions_lex_less) order the rare runs whose keys
+// tie exactly. Only paths equal in every compared field can come out in another order
+// than the reference's std::sort (whose order for them is unspecified).
+struct ExactView {
+  uint32_t stride;
+  const uint32_t *src, *tx, *rx, *ni, *label;
+  const uint8_t* kind;
+  const double *pos, *txp, *len, *delay;
+  __device__ uint32_t k(uint32_t e) const { return src[e]; }
+};
+
+__device__ __forceinline__ uint64_t mix64d(uint64_t h, uint64_t v) {
+  h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  h *= 0xff51afd7ed558ccdull;
+  h ^= h >> 33;
+  return h;
 }
 
-// dedup_by_label, dedup_by_fresnel, final order (pipeline.cpp:189-207) -> S->paths
-void finish_paths(std::vector<EP> exact, const pcr_run_config& cfg, pcr_summary* S) {
-  exact = dedup_by_label(std::move(exact));
-  if (cfg.fresnel_enabled) exact = dedup_by_fresnel(std::move(exact), cfg.carrier_frequency_hz);
-  final_sort(exact);
+// has_path -> exact-path list in candidate order; reject histogram; iteration sum
+__global__ void exact_flags_kernel(const uint8_t* __restrict__ has, const int32_t* __restrict__ reason,
+                                   const uint32_t* __restrict__ iters, uint32_t n, uint32_t* __restrict__ flag,
+                                   unsigned long long* __restrict__ counts /* 4 rejects, iterations */) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long it = 0;
+  if (i < n) {
+    flag[i] = has[i] ? 1u : 0u;
+    if (!has[i]) atomicAdd(counts + (reason[i] & 3), 1ull);
+    it = iters[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) it += __shfl_down_sync(0xffffffffu, it, o);
+  if ((threadIdx.x & 31) == 0 && it) atomicAdd(counts + 4, it);
+}
+
+__global__ void compact_idx_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, uint32_t n,
+                                   const uint32_t* __restrict__ in, uint32_t* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && flag[i]) out[pos[i]] = in ? in[i] : i;
+}
+
+// group keys of the exact paths listed in `ord`: 0 = (tx, rx, kinds, labels),
+// 1 = (tx, rx, kinds), 2 = delay bits, 3 = rx, 4 = tx
+__global__ void exact_key_kernel(ExactView v, const uint32_t* __restrict__ ord, uint32_t m, int what,
+                                 uint64_t* __restrict__ key) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const uint32_t k = v.k(ord[j]);
+  uint64_t r;
+  if (what <= 1) {
+    r = mix64d(mix64d(mix64d(0x51ed270b27u, v.tx[k]), v.rx[k]), v.ni[k]);
+    for (uint32_t q = 0; q < v.ni[k]; ++q) {
+      const size_t x = static_cast<size_t>(k) * v.stride + q;
+      r = mix64d(r, v.kind[x]);
+      if (what == 0) r = mix64d(r, v.label[x]);
+    }
+  } else if (what == 2) {
+    r = static_cast<uint64_t>(__double_as_longlong(v.delay[k]));  // delay >= 0: bits are ordered
+  } else {
+    r = what == 3 ? v.rx[k] : v.tx[k];
+  }
+  key[j] = r;
+}
+
+__device__ bool same_group(const ExactView& v, uint32_t ka, uint32_t kb, bool labels) {
+  if (v.tx[ka] != v.tx[kb] || v.rx[ka] != v.rx[kb] || v.ni[ka] != v.ni[kb]) return false;
+  for (uint32_t q = 0; q < v.ni[ka]; ++q) {
+    const size_t a = static_cast<size_t>(ka) * v.stride + q, b = static_cast<size_t>(kb) * v.stride + q;
+    if (v.kind[a] != v.kind[b]) return false;
+    if (labels && v.label[a] != v.label[b]) return false;
+  }
+  return true;
+}
+
+// run heads of equal keys in `ord` order; a key run that mixes groups is a hash collision
+__global__ void group_heads_kernel(ExactView v, const uint32_t* __restrict__ ord, const uint64_t* __restrict__ key,
+                                   uint32_t m, bool labels, uint32_t* __restrict__ head, int* __restrict__ collision) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const bool h = j == 0 || key[j] != key[j - 1];
+  head[j] = h ? 1u : 0u;
+  if (!h && !same_group(v, v.k(ord[j]), v.k(ord[j - 1]), labels)) *collision = 1;
+}
+
+// positions_lex_less (refine.cpp:304-311)
+__device__ bool dev_positions_lex_less(const ExactView& v, uint32_t ka, uint32_t kb) {
+  const uint32_t na = v.ni[ka], nb = v.ni[kb];
+  for (uint32_t q = 0; q < (na < nb ? na : nb); ++q) {
+    const double* a = v.pos + 3 * (static_cast<size_t>(ka) * v.stride + q);
+    const double* b = v.pos + 3 * (static_cast<size_t>(kb) * v.stride + q);
+    if (a[0] != b[0] || a[1] != b[1] || a[2] != b[2]) {
+      if (a[0] != b[0]) return a[0] < b[0];
+      if (a[1] != b[1]) return a[1] < b[1];
+      return a[2] < b[2];
+    }
+  }
+  return na < nb;
+}
+
+// dedup_by_label's winner per group: runs are in candidate order, the candidate
+// replaces the current best only when strictly better (length, then positions)
+__global__ void label_winner_kernel(ExactView v, const uint32_t* __restrict__ ord, const uint32_t* __restrict__ head_pos,
+                                    uint32_t n_groups, uint32_t m, uint32_t* __restrict__ winner) {
+  const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= n_groups) return;
+  const uint32_t b = head_pos[gi], e = gi + 1 < n_groups ? head_pos[gi + 1] : m;
+  uint32_t best = ord[b];
+  for (uint32_t j = b + 1; j < e; ++j) {
+    const uint32_t c = ord[j];
+    const uint32_t kc = v.k(c), kb = v.k(best);
+    if (v.len[kc] < v.len[kb] || (v.len[kc] == v.len[kb] && dev_positions_lex_less(v, kc, kb))) best = c;
+  }
+  winner[gi] = best;
+}
+
+// dedup_by_fresnel within one (tx, rx, kinds) bucket, members in delay order: a path
+// is a duplicate when all its points lie inside the first-Fresnel ellipsoids of an
+// earlier kept path's incoming legs (refine.cpp:356-366)
+__global__ void fresnel_kernel(ExactView v, const uint32_t* __restrict__ ord, const uint32_t* __restrict__ head_pos,
+                               uint32_t n_groups, uint32_t m, double half_lambda, uint8_t* __restrict__ kept) {
+  const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= n_groups) return;
+  const uint32_t b = head_pos[gi], e = gi + 1 < n_groups ? head_pos[gi + 1] : m;
+  for (uint32_t j = b; j < e; ++j) {
+    const uint32_t kp = v.k(ord[j]);
+    bool dup = false;
+    for (uint32_t i = b; i < j && !dup; ++i) {
+      if (!kept[i]) continue;
+      const uint32_t kq = v.k(ord[i]);
+      bool inside = true;
+      for (uint32_t q = 0; q < v.ni[kp] && inside; ++q) {
+        const V3 a = q == 0 ? load3(v.txp + 3ull * kq) : load3(v.pos + 3 * (static_cast<size_t>(kq) * v.stride + q - 1));
+        const V3 bq = load3(v.pos + 3 * (static_cast<size_t>(kq) * v.stride + q));
+        const V3 pt = load3(v.pos + 3 * (static_cast<size_t>(kp) * v.stride + q));
+        inside = norm(pt - a) + norm(pt - bq) <= norm(bq - a) + half_lambda;
+      }
+      dup = inside;
+    }
+    kept[j] = dup ? 0 : 1;
+  }
+}
+
+__global__ void gather_u32_kernel(const uint32_t* __restrict__ src, const uint32_t* __restrict__ perm, uint32_t n,
+                                  uint32_t* __restrict__ dst) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[perm[i]];
+}
+
+__global__ void u8_to_u32_kernel(const uint8_t* __restrict__ a, uint32_t n, uint32_t* __restrict__ b) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = a[i];
+}
+
+// Runs of exactly tied sort keys get the comparator's remaining fields by an
+// insertion sort (runs are tiny): mode 0 = sort_by_delay's positions_lex_less over
+// equal (delay, tx, rx); mode 1 = the final order's (size, positions) over equal
+// (tx, rx, delay).
+__device__ __forceinline__ bool same_delay_key(const ExactView& v, uint32_t a, uint32_t b) {
+  const uint32_t ka = v.k(a), kb = v.k(b);
+  return v.delay[ka] == v.delay[kb] && v.tx[ka] == v.tx[kb] && v.rx[ka] == v.rx[kb];
+}
+
+// run heads of exactly tied (delay, tx, rx) keys, computed before any run is reordered
+__global__ void tie_heads_kernel(ExactView v, const uint32_t* __restrict__ ord, uint32_t m,
+                                 uint8_t* __restrict__ head) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  head[j] = (j == 0 || !same_delay_key(v, ord[j - 1], ord[j])) ? 1 : 0;
+}
+
+__global__ void tie_sort_kernel(ExactView v, uint32_t* __restrict__ ord, const uint8_t* __restrict__ head, uint32_t m,
+                                int mode) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m || !head[j]) return;
+  uint32_t e = j + 1;
+  while (e < m && !head[e]) ++e;
+  if (e - j < 2) return;
+  for (uint32_t x = j + 1; x < e; ++x) {
+    const uint32_t c = ord[x];
+    const uint32_t kc = v.k(c);
+    uint32_t y = x;
+    while (y > j) {
+      const uint32_t kp = v.k(ord[y - 1]);
+      const bool less = (mode == 1 && v.ni[kc] != v.ni[kp]) ? v.ni[kc] < v.ni[kp] : dev_positions_lex_less(v, kc, kp);
+      if (!less) break;
+      ord[y] = ord[y - 1];
+      --y;
+    }
+    ord[y] = c;
+  }
+}
+
+// Order runs of exactly tied (delay, tx, rx) keys by the comparator's remaining fields
+// (mode 0: positions_lex_less of sort_by_delay; mode 1: size then positions, final order).
+void sort_ties(Ctx& ctx, const ExactView& v, DBuf<uint32_t>& ord, uint32_t m, int mode) {
+  if (m < 2) return;
+  cudaStream_t s = ctx.stream;
+  DBuf<uint8_t> head(m, s);
+  count_launch();
+  tie_heads_kernel<<<nb(m), 256, 0, s>>>(v, ord.get(), m, head.get());
+  PCR_LAUNCH_CHECK();
+  count_launch();
+  tie_sort_kernel<<<nb(m), 256, 0, s>>>(v, ord.get(), head.get(), m, mode);
+  PCR_LAUNCH_CHECK();
+}
+
+__global__ void scatter_flag_kernel(const uint32_t* __restrict__ ord, const uint32_t* __restrict__ f, uint32_t n,
+                                    uint32_t* __restrict__ by_id) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) by_id[ord[i]] = f[i];
+}
+
+__global__ void gather_exact_kernel(const uint32_t* __restrict__ rows, uint32_t m, uint32_t st,
+                                    const uint32_t* tx, const uint32_t* rx, const uint32_t* ni, const double* txp,
+                                    const double* rxp, const double* len, const double* del, const double* gn,
+                                    const uint8_t* kind, const double* pos, const double* nrm, const uint32_t* lab,
+                                    const uint32_t* ie, const uint32_t* ed, uint32_t* o_tx, uint32_t* o_rx,
+                                    uint32_t* o_ni, double* o_txp, double* o_rxp, double* o_len, double* o_del,
+                                    double* o_gn, uint8_t* o_kind, double* o_pos, double* o_nrm, uint32_t* o_lab,
+                                    uint32_t* o_ie, uint32_t* o_ed) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const uint32_t k = rows[i];
+  o_tx[i] = tx[k];
+  o_rx[i] = rx[k];
+  o_ni[i] = ni[k];
+  for (int a = 0; a < 3; ++a) {
+    o_txp[3ull * i + a] = txp[3ull * k + a];
+    o_rxp[3ull * i + a] = rxp[3ull * k + a];
+  }
+  o_len[i] = len[k];
+  o_del[i] = del[k];
+  o_gn[i] = gn[k];
+  for (uint32_t q = 0; q < st; ++q) {
+    const size_t d = static_cast<size_t>(i) * st + q, sidx = static_cast<size_t>(k) * st + q;
+    o_kind[d] = kind[sidx];
+    o_lab[d] = lab[sidx];
+    o_ie[d] = ie[sidx];
+    o_ed[d] = ed[sidx];
+    for (int a = 0; a < 3; ++a) {
+      o_pos[3 * d + a] = pos[3 * sidx + a];
+      o_nrm[3 * d + a] = nrm[3 * sidx + a];
+    }
+  }
+}
+
+// Stable sort of `ord` (m exact-path ids) by key `what` (see exact_key_kernel).
+void sort_by(Ctx& ctx, const ExactView& v, DBuf<uint32_t>& ord, uint32_t m, int what, int bits) {
+  if (m < 2) return;
+  cudaStream_t s = ctx.stream;
+  DBuf<uint64_t> key(m, s);
+  count_launch();
+  exact_key_kernel<<<nb(m), 256, 0, s>>>(v, ord.get(), m, what, key.get());
+  PCR_LAUNCH_CHECK();
+  radix_sort_pairs(key.get(), ord.get(), m, 0, bits, s);
+}
+
+// Group `ord` (already in the wanted in-group order) by key `what`, stable: returns
+// the group head positions.
+std::vector<uint32_t> group_by(Ctx& ctx, const ExactView& v, DBuf<uint32_t>& ord, uint32_t m, int what,
+                               DBuf<uint32_t>& heads) {
+  cudaStream_t s = ctx.stream;
+  DBuf<uint64_t> key(m ? m : 1, s);
+  if (m) {
+    count_launch();
+    exact_key_kernel<<<nb(m), 256, 0, s>>>(v, ord.get(), m, what, key.get());
+    PCR_LAUNCH_CHECK();
+    radix_sort_pairs(key.get(), ord.get(), m, 0, 64, s);
+  }
+  DBuf<uint32_t> head(m ? m : 1, s), pos(m ? m : 1, s), tot(1, s);
+  DBuf<int> coll(1, s);
+  PCR_CUDA(cudaMemsetAsync(coll.get(), 0, sizeof(int), s));
+  PCR_CUDA(cudaMemsetAsync(tot.get(), 0, sizeof(uint32_t), s));
+  if (m) {
+    count_launch();
+    group_heads_kernel<<<nb(m), 256, 0, s>>>(v, ord.get(), key.get(), m, what == 0, head.get(), coll.get());
+    PCR_LAUNCH_CHECK();
+    exclusive_scan_u32(head.get(), pos.get(), m, tot.get(), s);
+  }
+  uint32_t ng = 0;
+  int c = 0;
+  d2h(&ng, tot.get(), 1, s);
+  d2h(&c, coll.get(), 1, s);
+  PCR_CUDA(cudaStreamSynchronize(s));
+  if (c) throw Error(4, "dedup: group hash collision");
+  heads.alloc(ng ? ng : 1, s);
+  if (m) {
+    count_launch();
+    compact_idx_kernel<<<nb(m), 256, 0, s>>>(head.get(), pos.get(), m, nullptr, heads.get());
+    PCR_LAUNCH_CHECK();
+  }
+  return {ng};
+}
+
+// Refinement outcomes -> deduplicated exact paths in the final order (host EPs), with
+// the refine counters (refined_paths, rejected, refine_iterations).
+std::vector<EP> dedup_device(Ctx& ctx, const CandSet& cs, const RefineDevOut& ro, const pcr_run_config& cfg,
+                             pcr_summary* S) {
+  cudaStream_t s = ctx.stream;
+  const uint32_t n = cs.n;
+  // exact paths (has_path) in candidate order
+  DBuf<uint32_t> flag(n ? n : 1, s), fpos(n ? n : 1, s), tot(1, s);
+  DBuf<unsigned long long> counts(5, s);
+  PCR_CUDA(cudaMemsetAsync(counts.get(), 0, 5 * sizeof(unsigned long long), s));
+  PCR_CUDA(cudaMemsetAsync(tot.get(), 0, sizeof(uint32_t), s));
+  if (n) {
+    count_launch();
+    exact_flags_kernel<<<nb(n), 256, 0, s>>>(ro.has_path.get(), ro.reason.get(), ro.iters.get(), n, flag.get(),
+                                              counts.get());
+    PCR_LAUNCH_CHECK();
+    exclusive_scan_u32(flag.get(), fpos.get(), n, tot.get(), s);
+  }
+  uint32_t m = 0;
+  unsigned long long hc[5];
+  d2h(&m, tot.get(), 1, s);
+  d2h(hc, counts.get(), 5, s);
+  PCR_CUDA(cudaStreamSynchronize(s));
+  for (int r = 0; r < 4; ++r) S->rejected[r] = hc[r];
+  S->refine_iterations = hc[4];
+  S->refined_paths = m;
+  DBuf<uint32_t> src(m ? m : 1, s);
+  if (n) {
+    count_launch();
+    compact_idx_kernel<<<nb(n), 256, 0, s>>>(flag.get(), fpos.get(), n, nullptr, src.get());
+    PCR_LAUNCH_CHECK();
+  }
+  const ExactView v{cs.stride,      src.get(),     cs.tx_id.get(), cs.rx_id.get(), cs.n_inter.get(),
+                    ro.label.get(), cs.kind.get(), ro.pos.get(),   cs.tx_pos.get(), ro.length.get(),
+                    ro.delay.get()};
+  // dedup_by_label: groups in candidate order, strict-improvement winner per group
+  DBuf<uint32_t> ord(m ? m : 1, s), heads;
+  iota_u32(ord.get(), m, s);
+  uint32_t ng = group_by(ctx, v, ord, m, 0, heads)[0];
+  DBuf<uint32_t> kept(ng ? ng : 1, s);
+  if (ng) {
+    count_launch();
+    label_winner_kernel<<<nb(ng), 256, 0, s>>>(v, ord.get(), heads.get(), ng, m, kept.get());
+    PCR_LAUNCH_CHECK();
+  }
+  // sort_by_delay: (delay, tx, rx) by stable LSD passes, positions on the host below
+  sort_by(ctx, v, kept, ng, 3, 32);
+  sort_by(ctx, v, kept, ng, 4, 32);
+  sort_by(ctx, v, kept, ng, 2, 64);
+  sort_ties(ctx, v, kept, ng, 0);
+  uint32_t mf = ng;
+  DBuf<uint32_t> fin;
+  if (cfg.fresnel_enabled && ng) {
+    // dedup_by_fresnel: buckets (tx, rx, kinds), members in delay order
+    DBuf<uint32_t> b_ord(ng, s), b_heads;
+    PCR_CUDA(cudaMemcpyAsync(b_ord.get(), kept.get(), ng * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    const uint32_t nb_ = group_by(ctx, v, b_ord, ng, 1, b_heads)[0];
+    DBuf<uint8_t> keep8(ng, s);
+    count_launch();
+    fresnel_kernel<<<nb(nb_, 128), 128, 0, s>>>(v, b_ord.get(), b_heads.get(), nb_, ng,
+                                                 0.5 * (kC / cfg.carrier_frequency_hz), keep8.get());
+    PCR_LAUNCH_CHECK();
+    // survivors back in delay order: flag by path id, then compact the delay order
+    DBuf<uint32_t> k32(ng, s), by_id(m ? m : 1, s), f2(ng, s), p2(ng, s), t2(1, s);
+    PCR_CUDA(cudaMemsetAsync(by_id.get(), 0, (m ? m : 1) * sizeof(uint32_t), s));
+    count_launch();
+    u8_to_u32_kernel<<<nb(ng), 256, 0, s>>>(keep8.get(), ng, k32.get());
+    PCR_LAUNCH_CHECK();
+    count_launch();
+    scatter_flag_kernel<<<nb(ng), 256, 0, s>>>(b_ord.get(), k32.get(), ng, by_id.get());
+    PCR_LAUNCH_CHECK();
+    count_launch();
+    gather_u32_kernel<<<nb(ng), 256, 0, s>>>(by_id.get(), kept.get(), ng, f2.get());
+    PCR_LAUNCH_CHECK();
+    exclusive_scan_u32(f2.get(), p2.get(), ng, t2.get(), s);
+    d2h(&mf, t2.get(), 1, s);
+    PCR_CUDA(cudaStreamSynchronize(s));
+    fin.alloc(mf ? mf : 1, s);
+    count_launch();
+    compact_idx_kernel<<<nb(ng), 256, 0, s>>>(f2.get(), p2.get(), ng, kept.get(), fin.get());
+    PCR_LAUNCH_CHECK();
+  } else {
+    fin.swap(kept);
+  }
+  // final order (pipeline.cpp:194-207): (tx, rx, delay) by stable passes over the
+  // delay-ordered survivors; (size, positions) on the host for exact key ties
+  sort_by(ctx, v, fin, mf, 3, 32);
+  sort_by(ctx, v, fin, mf, 4, 32);
+  sort_ties(ctx, v, fin, mf, 1);
+  // download only the survivors
+  std::vector<uint32_t> ids(mf);
+  d2h(ids.data(), fin.get(), mf, s);
+  std::vector<uint32_t> hsrc(m);
+  d2h(hsrc.data(), src.get(), m, s);
+  PCR_CUDA(cudaStreamSynchronize(s));
+  const uint32_t stv = cs.stride;
+  std::vector<EP> out(mf);
+  {
+    // gather the survivors' rows on the device, then one copy per field
+    DBuf<uint32_t> rows(mf ? mf : 1, s);
+    std::vector<uint32_t> hrows(mf);
+    for (uint32_t i = 0; i < mf; ++i) hrows[i] = hsrc[ids[i]];
+    h2d(rows.get(), hrows.data(), mf, s);
+    DBuf<uint32_t> g_tx(mf + 1, s), g_rx(mf + 1, s), g_ni(mf + 1, s), g_lab(mf * stv + 1, s), g_ie(mf * stv + 1, s),
+        g_ed(mf * stv + 1, s);
+    DBuf<uint8_t> g_kind(mf * stv + 1, s);
+    DBuf<double> g_txp(3 * mf + 3, s), g_rxp(3 * mf + 3, s), g_len(mf + 1, s), g_del(mf + 1, s), g_gn(mf + 1, s),
+        g_pos(3 * mf * stv + 3, s), g_nrm(3 * mf * stv + 3, s);
+    if (mf) {
+      count_launch();
+      gather_exact_kernel<<<nb(mf), 256, 0, s>>>(
+          rows.get(), mf, stv, cs.tx_id.get(), cs.rx_id.get(), cs.n_inter.get(), cs.tx_pos.get(), cs.rx_pos.get(),
+          ro.length.get(), ro.delay.get(), ro.gnorm.get(), cs.kind.get(), ro.pos.get(), ro.nrm.get(), ro.label.get(),
+          cs.ie.get(), cs.edge.get(), g_tx.get(), g_rx.get(), g_ni.get(), g_txp.get(), g_rxp.get(), g_len.get(),
+          g_del.get(), g_gn.get(), g_kind.get(), g_pos.get(), g_nrm.get(), g_lab.get(), g_ie.get(), g_ed.get());
+      PCR_LAUNCH_CHECK();
+    }
+    std::vector<uint32_t> tx(mf), rx(mf), ni(mf), lab(mf * stv), ie(mf * stv), ed(mf * stv);
+    std::vector<uint8_t> kind(mf * stv);
+    std::vector<double> txp(3 * mf), rxp(3 * mf), len(mf), del(mf), gn(mf), pos(3 * mf * stv), nrm(3 * mf * stv);
+    d2h(tx.data(), g_tx.get(), mf, s);
+    d2h(rx.data(), g_rx.get(), mf, s);
+    d2h(ni.data(), g_ni.get(), mf, s);
+    d2h(txp.data(), g_txp.get(), 3 * mf, s);
+    d2h(rxp.data(), g_rxp.get(), 3 * mf, s);
+    d2h(len.data(), g_len.get(), mf, s);
+    d2h(del.data(), g_del.get(), mf, s);
+    d2h(gn.data(), g_gn.get(), mf, s);
+    d2h(kind.data(), g_kind.get(), mf * stv, s);
+    d2h(pos.data(), g_pos.get(), 3 * mf * stv, s);
+    d2h(nrm.data(), g_nrm.get(), 3 * mf * stv, s);
+    d2h(lab.data(), g_lab.get(), mf * stv, s);
+    d2h(ie.data(), g_ie.get(), mf * stv, s);
+    d2h(ed.data(), g_ed.get(), mf * stv, s);
+    PCR_CUDA(cudaStreamSynchronize(s));
+    for (uint32_t i = 0; i < mf; ++i) {
+      EP& e = out[i];
+      e.tx_id = tx[i];
+      e.rx_id = rx[i];
+      e.tx = load3(&txp[3 * i]);
+      e.rx = load3(&rxp[3 * i]);
+      e.total_length = len[i];
+      e.delay = del[i];
+      e.gnorm = gn[i];
+      e.converged = true;
+      for (uint32_t q = 0; q < ni[i]; ++q) {
+        const size_t j = static_cast<size_t>(i) * stv + q;
+        e.its.push_back(It{kind[j], load3(&pos[3 * j]), load3(&nrm[3 * j]), lab[j], ie[j], ed[j]});
+      }
+    }
+  }
+  return out;
+}
+
+// the final paths -> S->paths
+void emit_paths(const std::vector<EP>& exact, pcr_summary* S) {
   S->exact_paths = exact.size();
   size_t st = 1;
   for (const EP& e : exact) st = std::max(st, e.its.size());
@@ -661,20 +959,23 @@ void run_pipeline_core(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cf
 
   // refine
   t0 = Clock::now();
-  std::vector<EP> exact;
+  RefineDevOut ro;
   try {
-    RefineDevOut ro;
     refine_cands(ctx, grid, scene, cs, cfg, 0, 1, ro);
     S->refine_trials = ro.trials;
     S->refine_marches = ro.marches;
-    exact = collect_paths(ctx, cs, ro, S);
   } catch (const std::exception& e) {
     stage_fail("refine", e);
   }
   run.timing("refine", since(t0));
 
+  // dedup_by_label, dedup_by_fresnel and the final order, on the device
   t0 = Clock::now();
-  finish_paths(std::move(exact), cfg, S);
+  try {
+    emit_paths(dedup_device(ctx, cs, ro, cfg, S), S);
+  } catch (const std::exception& e) {
+    stage_fail("refine", e);
+  }
   run.timing("dedup", since(t0));
   *out = run.release();
 }
@@ -926,10 +1227,9 @@ void api_shard_finish(Ctx& ctx, const void* rows, uint64_t n_rows, const pcr_sha
   S->refine_trials = totals.refine_trials;
   S->refine_marches = totals.refine_marches;
   run.timing("trace", st.trace_s);
-  std::vector<EP> exact;
+  RefineDevOut ro;
   try {
     if (n_rows != cs.n) throw Error(PCR_ERR_INVALID, "shard: outcome rows do not cover the candidate list");
-    RefineDevOut ro;
     const size_t m = cs.n ? cs.n : 1, ms = m * stride;
     ro.reason.alloc(m, s);
     ro.has_path.alloc(m, s);
@@ -957,13 +1257,16 @@ void api_shard_finish(Ctx& ctx, const void* rows, uint64_t n_rows, const pcr_sha
     d2h(&h_bad, bad.get(), 1, s);
     PCR_CUDA(cudaStreamSynchronize(s));
     if (h_bad) throw Error(PCR_ERR_INVALID, "shard: outcome rows do not cover the candidate list");
-    exact = collect_paths(ctx, cs, ro, S);
   } catch (const std::exception& e) {
     stage_fail("refine", e);
   }
   run.timing("refine", st.refine_s + since(t0));
   t0 = Clock::now();
-  finish_paths(std::move(exact), st.cfg, S);
+  try {
+    emit_paths(dedup_device(ctx, cs, ro, st.cfg, S), S);
+  } catch (const std::exception& e) {
+    stage_fail("refine", e);
+  }
   run.timing("dedup", since(t0));
   *out = run.release();
 }

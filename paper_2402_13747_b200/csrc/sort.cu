@@ -15,6 +15,14 @@ namespace pcr {
 
 uint64_t g_launch_count = 0, g_h2d_bytes = 0, g_d2h_bytes = 0;
 
+bool sync_launches() {
+  static const bool on = [] {
+    const char* e = std::getenv("PCR_SYNC_LAUNCHES");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 namespace {
 
 constexpr int kScanThreads = 256;
