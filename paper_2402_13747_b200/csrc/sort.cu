@@ -147,24 +147,31 @@ __global__ void __launch_bounds__(kRadixThreads) radix_upsweep(const uint64_t* _
   counts[static_cast<size_t>(threadIdx.x) * n_tiles + blockIdx.x] = hist[threadIdx.x];
 }
 
+// One tile: rank every key within its digit (warp match + per-warp counters), place
+// the tile digit-sorted in shared memory, then write it out run by run so consecutive
+// threads store consecutive addresses of one digit's output range (coalesced). The
+// order within a digit stays the input order: the sort is stable.
 __global__ void __launch_bounds__(kRadixThreads) radix_downsweep(
     const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint64_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, size_t n, int shift, const uint32_t* __restrict__ offsets, uint32_t n_tiles) {
   __shared__ uint32_t cnt[kRadixWarps][kRadixDigits];
+  __shared__ uint32_t dstart[kRadixDigits];
+  __shared__ uint64_t stage[kRadixTile];  // keys, then (reused) values
+  __shared__ uint8_t sdig[kRadixTile];
   for (int i = threadIdx.x; i < kRadixWarps * kRadixDigits; i += kRadixThreads) (&cnt[0][0])[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const size_t base = static_cast<size_t>(blockIdx.x) * kRadixTile + static_cast<size_t>(wid) * 32 * kRadixIpt;
+  const size_t tile0 = static_cast<size_t>(blockIdx.x) * kRadixTile;
+  const size_t base = tile0 + static_cast<size_t>(wid) * 32 * kRadixIpt;
+  const uint32_t tile_n = static_cast<uint32_t>(n - tile0 < static_cast<size_t>(kRadixTile) ? n - tile0 : kRadixTile);
   uint64_t key[kRadixIpt];
-  uint32_t val[kRadixIpt];
   uint32_t loc[kRadixIpt];
 #pragma unroll
   for (int k = 0; k < kRadixIpt; ++k) {
     const size_t i = base + static_cast<size_t>(k) * 32 + lane;
     const bool ok = i < n;
     key[k] = ok ? keys_in[i] : 0ull;
-    val[k] = ok ? vals_in[i] : 0u;
     const uint32_t d = ok ? static_cast<uint32_t>((key[k] >> shift) & 0xffu) : (0x100u + lane);
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const uint32_t rank = __popc(peers & lt_mask);
@@ -177,6 +184,7 @@ __global__ void __launch_bounds__(kRadixThreads) radix_downsweep(
   }
   __syncthreads();
   {
+    // per digit: exclusive over warps, then the digit's start within the tile
     const int d = threadIdx.x;  // one digit per thread
     uint32_t run = 0;
 #pragma unroll
@@ -185,17 +193,48 @@ __global__ void __launch_bounds__(kRadixThreads) radix_downsweep(
       cnt[w][d] = run;
       run += t;
     }
+    // block exclusive scan of the digit totals (256 threads = 256 digits)
+    uint32_t incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    __shared__ uint32_t wsum[kRadixWarps];
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    uint32_t woff = 0;
+    for (int w = 0; w < wid; ++w) woff += wsum[w];
+    dstart[d] = woff + incl - run;
   }
   __syncthreads();
+  uint32_t lpos[kRadixIpt];
 #pragma unroll
   for (int k = 0; k < kRadixIpt; ++k) {
     const size_t i = base + static_cast<size_t>(k) * 32 + lane;
     if (i < n) {
       const uint32_t d = static_cast<uint32_t>((key[k] >> shift) & 0xffu);
-      const size_t pos = static_cast<size_t>(offsets[static_cast<size_t>(d) * n_tiles + blockIdx.x]) + cnt[wid][d] + loc[k];
-      keys_out[pos] = key[k];
-      vals_out[pos] = val[k];
+      lpos[k] = dstart[d] + cnt[wid][d] + loc[k];
+      stage[lpos[k]] = key[k];
+      sdig[lpos[k]] = static_cast<uint8_t>(d);
     }
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < tile_n; j += kRadixThreads) {
+    const uint32_t d = sdig[j];
+    keys_out[static_cast<size_t>(offsets[static_cast<size_t>(d) * n_tiles + blockIdx.x]) + (j - dstart[d])] = stage[j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kRadixIpt; ++k) {
+    const size_t i = base + static_cast<size_t>(k) * 32 + lane;
+    if (i < n) reinterpret_cast<uint32_t*>(stage)[lpos[k]] = vals_in[i];
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < tile_n; j += kRadixThreads) {
+    const uint32_t d = sdig[j];
+    vals_out[static_cast<size_t>(offsets[static_cast<size_t>(d) * n_tiles + blockIdx.x]) + (j - dstart[d])] =
+        reinterpret_cast<const uint32_t*>(stage)[j];
   }
 }
 
