@@ -181,12 +181,19 @@ def b200_arm(args, rank, world, local_rank):
 
     from paper_2402_13747_b200 import abi, pcray, scenes, shard
 
-    torch.cuda.set_device(local_rank)
+    # one GPU per rank; --backend gloo on a box with fewer GPUs than ranks (a dry run of
+    # the N > 1 code path) places ranks round-robin — gloo's host-side collectives never
+    # make one rank's kernels wait on another's
+    dev = local_rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(args.backend)
 
     def barrier():
         if dist:
@@ -196,19 +203,19 @@ def b200_arm(args, rank, world, local_rank):
     def max_over_ranks(x):
         if not dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if args.backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x):
         if not dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if args.backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
     scene, cfg = scenes.build_scene(CONFIG)
-    ctx = pcray.Context(local_rank)
+    ctx = pcray.Context(dev)
     pcray.Context._default = ctx
     conf = abi.default_run_config(**cfg.run)
     ds = pcray.DeviceScene(scene, ctx)
@@ -250,7 +257,7 @@ def b200_arm(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     barrier()
-    with ClockSampler(local_rank) as clocks:
+    with ClockSampler(dev) as clocks:
         barrier()
         ms, outs, launches, _, ktimes = timed_steps(step, args.steps, profile=True)
         barrier()
@@ -328,7 +335,7 @@ def b200_arm(args, rank, world, local_rank):
                        "edges": int(len(scene.edges)), "max_interactions": cfg.run["max_interactions"],
                        "max_diffractions": cfg.run["max_diffractions"], "kappa": conf.kappa,
                        "parallelism": (f"{world} shards: initial hits and candidates split cyclically, "
-                                       "rows all-gathered over NCCL" if world > 1 else "single GPU"),
+                                       f"rows all-gathered over {args.backend.upper()}" if world > 1 else "single GPU"),
                        "l2": "flushed (256 MB write) before every timed step"},
             "rays_per_step": rays, "exact_paths_per_s": exact_per_s, "candidates_refined_per_s": cand_per_s,
             "exact_paths": s0["exact_paths"], "coarse_paths": s0["coarse_paths"],
@@ -354,6 +361,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU work for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"], help="N > 1 process group backend")
     args = ap.parse_args()
     rank, world, local_rank = dist_env()
     if args.impl == "reference":
