@@ -307,11 +307,15 @@ struct RefOut {
 // The iteration is a pure function of it, so a bitwise repeat means the trajectory
 // is periodic and can never reach ||g|| < delta (every state of the cycle already
 // failed the test) — the reference would spin to rho and report not_converged.
+// Every per-path array is sized by the kernel's depth bound D (the candidates' stride
+// rounded up to 3, 5 or 8), so the thread's local-memory frame stays small.
+template <int D>
 struct Snapshot {
-  double v[kMaxDepth][7];
+  double v[D][7];
 };
 
-__device__ __forceinline__ void take_snapshot(Snapshot& sn, const RNode* nd, int d) {
+template <int D>
+__device__ __forceinline__ void take_snapshot(Snapshot<D>& sn, const RNode* nd, int d) {
   for (int q = 0; q < d; ++q) {
     if (nd[q].kind == 0) {
       sn.v[q][0] = nd[q].c.x;
@@ -327,7 +331,8 @@ __device__ __forceinline__ void take_snapshot(Snapshot& sn, const RNode* nd, int
   }
 }
 
-__device__ __forceinline__ bool same_snapshot(const Snapshot& sn, const RNode* nd, int d) {
+template <int D>
+__device__ __forceinline__ bool same_snapshot(const Snapshot<D>& sn, const RNode* nd, int d) {
   for (int q = 0; q < d; ++q) {
     if (nd[q].kind == 0) {
       if (__double_as_longlong(sn.v[q][0]) != __double_as_longlong(nd[q].c.x) ||
@@ -345,6 +350,7 @@ __device__ __forceinline__ bool same_snapshot(const Snapshot& sn, const RNode* n
   return true;
 }
 
+template <int D>
 __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const GridView& g, const SceneView& s,
                                            double delta, int rho, double step_size, const RefOut& o);
 
@@ -353,7 +359,8 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
 // the slowest lane of its warp is done.
 constexpr int kRefineThreads = 128;
 __device__ unsigned long long* g_refine_dbg = nullptr;
-__global__ void __launch_bounds__(kRefineThreads, 4) refine_kernel(CandIn in, uint32_t n, GridView g, SceneView s,
+template <int D, int kMinBlocks>
+__global__ void __launch_bounds__(kRefineThreads, kMinBlocks) refine_kernel(CandIn in, uint32_t n, GridView g, SceneView s,
                                                                    double delta, int rho, double step_size, RefOut o,
                                                                    uint32_t* next_cand, int rev) {
   uint32_t done = 0;
@@ -365,7 +372,7 @@ __global__ void __launch_bounds__(kRefineThreads, 4) refine_kernel(CandIn in, ui
     // this shard's candidates are first, first + step, ... (SURVEY 8e round-robin)
     // list order by default (measured faster than back to front, PCR_REFINE_REV=1:
     // neighbours in DFS order are similar paths, so a warp's lanes diverge less)
-    refine_one(in.first + (rev ? n - 1 - idx : idx) * in.step, in, g, s, delta, rho, step_size, o);
+    refine_one<D>(in.first + (rev ? n - 1 - idx : idx) * in.step, in, g, s, delta, rho, step_size, o);
     ++done;
   }
   if (g_refine_dbg) {  // development trace (PCR_REFINE_TRACE): per-thread finish time, paths
@@ -378,6 +385,7 @@ __global__ void __launch_bounds__(kRefineThreads, 4) refine_kernel(CandIn in, ui
   }
 }
 
+template <int D>
 __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const GridView& g, const SceneView& s,
                                            double delta, int rho, double step_size, const RefOut& o) {
   const int d = static_cast<int>(in.n_inter[k]);
@@ -393,7 +401,7 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
     o.gnorm[k] = 0.0;
     return;
   }
-  RNode nd[kMaxDepth];
+  RNode nd[D];
   // make_path_state (refine.cpp:134-161)
   for (int q = 0; q < d; ++q) {
     const size_t j = static_cast<size_t>(k) * in.stride + q;
@@ -418,7 +426,7 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
       x.n = V3{0, 0, 1};
     }
   }
-  V3 pts[kMaxDepth];
+  V3 pts[D];
   for (int q = 0; q < d; ++q) pts[q] = node_point(nd[q], nd[q].p0, nd[q].p1);
   double f = chain_len(tx, pts, d, rx);
   double gnorm = 0.0;
@@ -430,7 +438,7 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
     atomicAdd(o.stats + 1, static_cast<unsigned long long>(n_march));
   };
   // Brent cycle detection on the post-iteration state
-  Snapshot saved, last[2];  // Brent's saved state; the states 1 and 2 iterations back
+  Snapshot<D> saved, last[2];  // Brent's saved state; the states 1 and 2 iterations back
   take_snapshot(saved, nd, d);
   last[0] = saved;
   last[1] = saved;
@@ -438,7 +446,7 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
   bool stalled = false;
   for (; iter < rho; ++iter) {
     // local_gradients
-    double gr[2 * kMaxDepth];
+    double gr[2 * D];
     int ng = 0;
     for (int q = 0; q < d; ++q) {
       const V3 prev = q == 0 ? tx : pts[q - 1];
@@ -470,10 +478,10 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
     // backtracking (refine.cpp:209-232)
     double step = step_size;
     bool accepted = false;
-    double tp0[kMaxDepth], tp1[kMaxDepth];
+    double tp0[D], tp1[D];
     for (int h = 0; h <= 8; ++h) {
       int gi = 0;
-      V3 tpts[kMaxDepth];
+      V3 tpts[D];
       for (int q = 0; q < d; ++q) {
         if (nd[q].kind == 0) {
           tp0[q] = nd[q].p0 - step * gr[gi++];
@@ -719,7 +727,11 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     KTimer kt(ctx, "refine");
     // enough resident threads to fill every SM at the kernel's occupancy
     int per_sm = 0;
-    PCR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, kRefineThreads, 0));
+    // depth bound of this batch: the smallest instantiation that holds its stride
+    // (4 blocks of 128 threads per SM, 128 registers: measured faster than 168 or 255
+    // registers per thread, which cut the spill traffic but halve the resident warps)
+    auto kern = in.stride <= 3 ? refine_kernel<3, 4> : in.stride <= 5 ? refine_kernel<5, 4> : refine_kernel<kMaxDepth, 4>;
+    PCR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, 0));
     const uint64_t want = (static_cast<uint64_t>(n_sub) + kRefineThreads - 1) / kRefineThreads;
     const uint64_t cap = static_cast<uint64_t>(ctx.sm_count) * (per_sm > 0 ? per_sm : 1);
     const unsigned grid_n = static_cast<unsigned>(want < cap ? want : cap);
@@ -735,7 +747,7 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
       t0 = static_cast<unsigned long long>(std::chrono::duration_cast<std::chrono::nanoseconds>(
           std::chrono::system_clock::now().time_since_epoch()).count());
     }
-    refine_kernel<<<grid_n, kRefineThreads, 0, s>>>(
+    kern<<<grid_n, kRefineThreads, 0, s>>>(
         ci, n_sub, gv, scene.view(), p.delta, p.rho, p.step_size, ro, next.get(), rev_order());
     if (trace) {
       std::vector<unsigned long long> h(3ull * grid_n * kRefineThreads);
