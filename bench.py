@@ -113,6 +113,16 @@ BYTES_CELL = 16.0            # int4 VoxelCell record
 BYTES_IE = 72.0              # IE label + sphere (32) + reception point (32) + meta
 
 
+def measured_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from a committed ncu capture (profiles/ncu_traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)[kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def roofline(kernel, ms_total, launches, summary, mean_depth, peaks, peaks_kind, fp64_tflops):
     if kernel == "refine":
         flops = (summary["refine_trials"] * (FLOP_TRIAL_PER_NODE * mean_depth + FLOP_TRIAL_BASE)
@@ -121,7 +131,9 @@ def roofline(kernel, ms_total, launches, summary, mean_depth, peaks, peaks_kind,
         per_launch = flops / max(launches, 1)
         achieved = per_launch / (ms_total / max(launches, 1) * 1e-3) / 1e12
         return {"bound": "fp64", "kernel": kernel, "achieved": achieved, "peak": fp64_tflops, "unit": "TFLOP/s",
-                "frac": achieved / fp64_tflops if fp64_tflops else None, "traffic": None,
+                "frac": achieved / fp64_tflops if fp64_tflops else None, "traffic": measured_traffic(kernel),
+                "traffic_note": "DRAM bytes per launch (ncu, profiles/ncu_traffic.json): spilled local memory; "
+                                "the kernel's algorithmic inputs are L2-resident",
                 "algorithmic_per_launch": per_launch, "avg_launch_ms": ms_total / max(launches, 1),
                 "peak_source": "in-run non-FMA FP64 probe (pcr_fp64_probe); MEASURED_PEAKS.json has no FP64 figure"}
     # traversal kernels: bytes of cell and IE records the walk reads
