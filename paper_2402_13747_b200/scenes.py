@@ -269,6 +269,9 @@ def config(name: str) -> SceneConfig:
     if name == "C2":
         return SceneConfig("C2", office_planar(), 1545.0, 11, dict(max_interactions=3, max_diffractions=1),
                            "synthetic indoor office, 1M points, 1 TX / 64 RX, 3 interactions incl. <= 1 diffraction")
+    if name == "C2np":
+        return SceneConfig("C2np", office_planar(), 1545.0, 11, dict(max_interactions=3, max_diffractions=1),
+                           "C2 with every normal tilted by up to 1 deg (seeded): non-planar IEs, exp() SDF path")
     if name == "C3":
         return SceneConfig("C3", canyon_planar(), 625.0, 3, dict(max_interactions=3, max_diffractions=0),
                            "synthetic street canyon, 10M points, 4 TX / 256 RX, 3 reflections")
@@ -284,6 +287,24 @@ def scaled_density(cfg: SceneConfig, target_points: int) -> float:
     return target_points / area
 
 
+def jitter_normals(scene: Scene, max_deg: float, seed: int) -> Scene:
+    """Tilt every normal by a random angle in [0, max_deg] about a random axis
+    perpendicular to it; the result is renormalised."""
+    rng = np.random.default_rng(seed)
+    n = np.asarray(scene.normal, dtype=np.float64)
+    a = rng.normal(size=n.shape)
+    a -= (a * n).sum(1, keepdims=True) * n
+    a /= np.linalg.norm(a, axis=1, keepdims=True)
+    th = np.radians(rng.uniform(0.0, max_deg, size=(len(n), 1)))
+    out = n * np.cos(th) + a * np.sin(th)
+    out /= np.linalg.norm(out, axis=1, keepdims=True)
+    return Scene(scene.position, out, scene.label, scene.edges, scene.edge_label, scene.tx, scene.tx_id, scene.rx,
+                 scene.rx_id, scene.carrier_frequency_hz)
+
+
 def build_scene(name: str, density: float | None = None) -> tuple[Scene, SceneConfig]:
     cfg = config(name)
-    return scene_from_planar(cfg.planar, density or cfg.density, cfg.seed), cfg
+    scene = scene_from_planar(cfg.planar, density or cfg.density, cfg.seed)
+    if name == "C2np":
+        scene = jitter_normals(scene, 1.0, cfg.seed)
+    return scene, cfg

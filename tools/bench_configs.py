@@ -188,7 +188,7 @@ def ply_ingest(points, cpu):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="C1,C2,C3,C4")
+    ap.add_argument("--configs", default="C1,C2,C2np,C3,C4")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--c5", action="store_true")
     ap.add_argument("--ply", type=int, default=0, help="PLY ingest benchmark with this many points")
