@@ -1,6 +1,9 @@
 #!/bin/bash
-# A/B the library builds in gpurun_out/ab on one command (development aid)
-for v in base payload; do
-  cp abtmp/$v.so paper_2402_13747_b200/libpcray_b200.so
-  echo "== $v"; eval "$1"
+# A/B of library builds on one gpurun call (development aid): copy each variant to
+# abtmp/<name>.so (git-ignored, travels with the snapshot), then
+#   tools/ab_libs.sh "<command>" name1 name2 ...
+cmd="$1"; shift
+for v in "$@"; do
+  cp "abtmp/$v.so" paper_2402_13747_b200/libpcray_b200.so
+  echo "== $v"; eval "$cmd"
 done
