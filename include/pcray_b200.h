@@ -350,6 +350,10 @@ int pcr_kernel_times(pcr_ctx* ctx, char (*names)[32], double* ms, uint64_t* laun
 /* measured non-FMA FP64 throughput of this device (TFLOP/s), the refinement roofline */
 int pcr_fp64_probe(pcr_ctx* ctx, double* tflops);
 
+/* the device exp() used by the non-planar SDF (estimate_surface), on host arrays:
+ * a parity hook — it equals the host libm's exp() bit for bit */
+int pcr_libm_exp_batch(pcr_ctx* ctx, const double* x, double* y, uint64_t n);
+
 /* config_hash (pipeline.hpp:39; pipeline.cpp:89-97) */
 uint64_t pcr_config_hash(const pcr_run_config* config);
 void pcr_run_config_defaults(pcr_run_config* config);

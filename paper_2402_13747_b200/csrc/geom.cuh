@@ -8,6 +8,7 @@
 #include <cstdint>
 
 #include "exact.cuh"
+#include "exp_table.cuh"
 
 namespace pcr {
 
@@ -93,8 +94,64 @@ struct SurfaceEstimate {
   double sdf, weight_sum;
 };
 
-// estimate_surface (surface.cpp:24-62). Non-planar payloads only; exp() is CUDA's
-// (<= 1 ulp from glibc's).
+// exp() as the host libm computes it (glibc >= 2.28's table-driven exp, in the FMA
+// build the x86-64 loader selects): k = round(x * 128/ln2), r = x - k ln2/128 in two
+// parts, exp(r) - 1 by a degree-5 polynomial, times 2^(k/128) from kExpTab, with the
+// scaled paths near overflow / underflow. The fused operations are explicit fma()
+// (the rest of the library is built without contraction). Equal to the host's exp()
+// bit for bit on 20M random arguments over its whole range (tools/gen_exp_table.py,
+// tests/test_nonplanar_gpu.py), which makes the non-planar SDF bit-exact.
+__device__ __forceinline__ double glibc_exp(double x) {
+  const double inv_ln2_n = 0x1.71547652b82fep0 * 128, neg_ln2_hi_n = -0x1.62e42fefa0000p-8,
+               neg_ln2_lo_n = -0x1.cf79abc9e3b3ap-47, shift = 0x1.8p52;
+  const double c2 = 0x1.ffffffffffdbdp-2, c3 = 0x1.555555555543cp-3, c4 = 0x1.55555cf172b91p-5,
+               c5 = 0x1.1111167a4d017p-7;
+  auto top12 = [](double v) { return static_cast<uint32_t>(static_cast<uint64_t>(__double_as_longlong(v)) >> 52); };
+  uint32_t abstop = top12(x) & 0x7ff;
+  if (abstop - top12(0x1p-54) >= top12(512.0) - top12(0x1p-54)) {
+    if (static_cast<int32_t>(abstop - top12(0x1p-54)) < 0) return 1.0 + x;  // |x| < 2^-54
+    if (abstop >= top12(1024.0)) {
+      if (__double_as_longlong(x) == __double_as_longlong(-__longlong_as_double(0x7ff0000000000000ll))) return 0.0;
+      if (abstop >= 0x7ff) return 1.0 + x;  // inf or nan
+      return (static_cast<uint64_t>(__double_as_longlong(x)) >> 63) ? 0.0
+                                                                     : __longlong_as_double(0x7ff0000000000000ll);
+    }
+    abstop = 0;  // large |x|: scaled below
+  }
+  double kd = fma(inv_ln2_n, x, shift);
+  const uint64_t ki = static_cast<uint64_t>(__double_as_longlong(kd));
+  kd -= shift;
+  const double r = fma(kd, neg_ln2_lo_n, fma(kd, neg_ln2_hi_n, x));
+  const uint64_t idx = 2 * (ki % 128);
+  const uint64_t top = ki << 45;
+  const double tail = __longlong_as_double(static_cast<long long>(kExpTab[idx]));
+  uint64_t sbits = kExpTab[idx + 1] + top;
+  const double r2 = r * r;
+  const double tmp = fma(r2 * r2, fma(r, c5, c4), fma(r2, fma(r, c3, c2), tail + r));
+  if (abstop != 0) {
+    const double scale = __longlong_as_double(static_cast<long long>(sbits));
+    return fma(scale, tmp, scale);
+  }
+  if ((ki & 0x80000000u) == 0) {  // k > 0: the scale's exponent may have overflowed
+    sbits -= 1009ull << 52;
+    const double scale = __longlong_as_double(static_cast<long long>(sbits));
+    return 0x1p1009 * fma(scale, tmp, scale);
+  }
+  sbits += 1022ull << 52;  // k < 0: round once before scaling into the subnormal range
+  const double scale = __longlong_as_double(static_cast<long long>(sbits));
+  double y = __dadd_rn(scale, __dmul_rn(scale, tmp));
+  if (y < 1.0) {
+    double lo = __dadd_rn(scale - y, __dmul_rn(scale, tmp));
+    const double hi = 1.0 + y;
+    lo = 1.0 - hi + y + lo;
+    y = (hi + lo) - 1.0;
+    if (y == 0.0) y = 0.0;
+  }
+  return 0x1p-1022 * y;
+}
+
+// estimate_surface (surface.cpp:24-62). Non-planar payloads only; exp() is the host
+// libm's (glibc_exp above).
 static __device__ __noinline__ SurfaceEstimate estimate_surface(const V3& x, uint32_t ie, const GridView& g,
                                                                 const SceneView& s) {
   const double h = g.sub_edge;
@@ -113,7 +170,7 @@ static __device__ __noinline__ SurfaceEstimate estimate_surface(const V3& x, uin
       best_d2 = d2;
       best = i;
     }
-    const double w = exp(-d2 * inv_h2);
+    const double w = glibc_exp(-d2 * inv_h2);
     w_sum += w;
     p_sum = p_sum + w * p;
     n_sum = n_sum + w * n;

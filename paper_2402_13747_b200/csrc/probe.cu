@@ -7,6 +7,7 @@
 #include "common.cuh"
 #include "../../include/pcray_b200.h"
 #include "device_state.cuh"
+#include "geom.cuh"
 
 namespace pcr {
 namespace {
@@ -23,6 +24,11 @@ __global__ void __launch_bounds__(256) fp64_probe_kernel(double* out, int iters,
 #pragma unroll
   for (int k = 0; k < 8; ++k) s += x[k];
   if (s == 12345.678) out[0] = s;  // keep the chains live
+}
+
+__global__ void libm_exp_kernel(const double* __restrict__ x, double* __restrict__ y, uint64_t n) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) y[i] = glibc_exp(x[i]);
 }
 
 }  // namespace
@@ -51,6 +57,29 @@ extern "C" int pcr_fp64_probe(pcr_ctx* ctx, double* tflops) {
     cudaEventDestroy(b);
     const double flops = 2.0 * 8.0 * iters * static_cast<double>(blocks) * threads;
     *tflops = flops / (ms * 1e-3) / 1e12;
+    return PCR_OK;
+  } catch (const std::exception& e) {
+    ctx->c.last_error = e.what();
+    return PCR_ERR_CUDA;
+  }
+}
+
+// The device exp() of the non-planar SDF on host arrays (parity hook: the tests compare
+// it with the host libm bit for bit).
+extern "C" int pcr_libm_exp_batch(pcr_ctx* ctx, const double* x, double* y, uint64_t n) {
+  if (!ctx || (n && (!x || !y))) return PCR_ERR_INVALID;
+  try {
+    PCR_CUDA(cudaSetDevice(ctx->c.device));
+    cudaStream_t s = ctx->c.stream;
+    pcr::DBuf<double> dx(n ? n : 1, s), dy(n ? n : 1, s);
+    pcr::h2d(dx.get(), x, n, s);
+    if (n) {
+      pcr::count_launch();
+      pcr::libm_exp_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(dx.get(), dy.get(), n);
+      PCR_LAUNCH_CHECK();
+    }
+    pcr::d2h(y, dy.get(), n, s);
+    PCR_CUDA(cudaStreamSynchronize(s));
     return PCR_OK;
   } catch (const std::exception& e) {
     ctx->c.last_error = e.what();

@@ -79,6 +79,7 @@ def lib():
         L.pcr_kernel_times.argtypes = [vp, vp, pp(C.c_double), pp(C.c_uint64), C.c_int, C.c_int]
         L.pcr_transfer_bytes.argtypes = [pp(C.c_uint64), pp(C.c_uint64)]
         L.pcr_fp64_probe.argtypes = [vp, pp(C.c_double)]
+        L.pcr_libm_exp_batch.argtypes = [vp, pp(C.c_double), pp(C.c_double), C.c_uint64]
         L.pcr_config_hash.restype = C.c_uint64
         L.pcr_config_hash.argtypes = [pp(abi.RunConfig)]
         L.pcr_run_config_defaults.argtypes = [pp(abi.RunConfig)]
@@ -100,7 +101,7 @@ EXPORTED_SYMBOLS = [
     "pcr_run_config_defaults", "pcr_free_paths", "pcr_free_initial_hits", "pcr_free_outcomes",
     "pcr_free_summary", "pcr_free_receptions", "pcr_run_pipeline_device", "pcr_shard_trace", "pcr_shard_rows",
     "pcr_shard_refine", "pcr_shard_outcomes", "pcr_shard_stats_get", "pcr_shard_finish", "pcr_scene_load_ply",
-    "pcr_scene_points", "pcr_write_paths",
+    "pcr_scene_points", "pcr_write_paths", "pcr_libm_exp_batch",
 ]
 
 
@@ -438,3 +439,13 @@ def fp64_probe(ctx: Context | None = None) -> float:
 def config_hash(config: RunConfig) -> int:
     """pcray::config_hash (pipeline.hpp:39)."""
     return int(lib().pcr_config_hash(C.byref(config)))
+
+
+def libm_exp(x, ctx: Context | None = None) -> np.ndarray:
+    """The device exp() of the non-planar SDF (pcr_libm_exp_batch), elementwise."""
+    ctx = ctx or Context.default()
+    a = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    out = np.zeros_like(a)
+    dp = C.POINTER(C.c_double)
+    ctx.check(lib().pcr_libm_exp_batch(ctx.handle, a.ctypes.data_as(dp), out.ctypes.data_as(dp), len(a)))
+    return out

@@ -62,8 +62,7 @@ def assert_bitwise(name, a, b):
 
 
 def assert_fp(name, a, b, exact=True, tol=1e-12):
-    """Bitwise for the planar hot path; within tol where the reference calls libm exp()
-    (non-planar SDF), integer fields always exact."""
+    """Bitwise unless exact=False (then within tol); integer fields always exact."""
     a = np.asarray(a)
     b = np.asarray(b)
     if exact or a.dtype != np.float64:
