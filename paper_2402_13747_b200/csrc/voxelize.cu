@@ -177,6 +177,10 @@ __global__ void surface_ie_kernel(const uint64_t* __restrict__ vs_key, const uin
                                   const double* __restrict__ nrm, SurfaceTmp t) {
   const int lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  // the round's positions staged per warp; lanes 0, 1, 2 then run the x, y and z sums,
+  // each sequential in point_indices order
+  __shared__ double stage[kThreads / 32][32][3];
+  double (*buf)[3] = stage[threadIdx.x >> 5];
   for (uint32_t ie = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ie < n_ie; ie += warps) {
     const uint32_t b = starts[ie];
     const uint32_t e = (ie + 1 < n_ie) ? starts[ie + 1] : static_cast<uint32_t>(n_pts);
@@ -197,13 +201,21 @@ __global__ void surface_ie_kernel(const uint64_t* __restrict__ vs_key, const uin
       }
       if (__any_sync(0xffffffffu, bad)) planar = false;
       const uint32_t cnt = min(32u, e - base);
-      for (uint32_t j = 0; j < cnt; ++j) {
-        const double x = __shfl_sync(0xffffffffu, p.x, j);
-        const double y = __shfl_sync(0xffffffffu, p.y, j);
-        const double z = __shfl_sync(0xffffffffu, p.z, j);
-        sum = sum + V3{x, y, z};
+      buf[lane][0] = p.x;
+      buf[lane][1] = p.y;
+      buf[lane][2] = p.z;
+      __syncwarp();
+      if (lane < 3) {
+        double acc = lane == 0 ? sum.x : lane == 1 ? sum.y : sum.z;
+        for (uint32_t j = 0; j < cnt; ++j) acc += buf[j][lane];
+        if (lane == 0) sum.x = acc;
+        else if (lane == 1) sum.y = acc;
+        else sum.z = acc;
       }
+      __syncwarp();
     }
+    sum.y = __shfl_sync(0xffffffffu, sum.y, 1);
+    sum.z = __shfl_sync(0xffffffffu, sum.z, 2);
     if (lane == 0) {
       const V3 c = sum / static_cast<double>(e - b);
       t.vs_key[ie] = vs_key[b];

@@ -16,4 +16,18 @@ ds = pcray.DeviceScene(scene)
 for _ in range(2):
     g = pcray.build_grid(ds, abi.voxel_params(vs, dv))
     del g
+if "--time" in sys.argv:
+    import torch
+
+    st = torch.cuda.ExternalStream(pcray.stream_ptr(ds.ctx))
+    ms = []
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        g = pcray.build_grid(ds, abi.voxel_params(vs, dv))
+        b.record(st)
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+        del g
+    print(f"build_grid {scene.n_points} points: min {min(ms):.3f} ms")
 print("done", scene.n_points)
