@@ -127,7 +127,7 @@ void exclusive_scan_impl(const T* in, T* out, size_t n, T* total_dev, cudaStream
 // ---------------------------------------------------------------------------------
 constexpr int kRadixThreads = 256;
 constexpr int kRadixWarps = kRadixThreads / 32;
-constexpr int kRadixIpt = 16;  // keys per thread
+constexpr int kRadixIpt = 8;  // keys per thread
 constexpr int kRadixTile = kRadixThreads * kRadixIpt;
 constexpr int kRadixDigits = 256;
 
