@@ -1,13 +1,15 @@
 // sort.cu — exclusive scan (reduce-then-scan) and a stable LSD radix sort.
 //
-// Radix pass (8-bit digits, 4096-key tiles, 256 threads = 8 warps):
+// Radix pass (8-bit digits, 2048-key tiles, 256 threads = 8 warps, 8 keys/thread):
 //   upsweep   : per-tile digit histogram -> counts[digit * n_tiles + tile]
 //   scan      : exclusive scan of counts (digit-major = global stable offsets)
-//   downsweep : each warp walks a contiguous 512-key run in 32-key chunks; peers
+//   downsweep : each warp walks a contiguous 256-key run in 32-key chunks; peers
 //               with the same digit are found with __match_any_sync, ranked by
 //               lane, and the warp's running per-digit count lives in shared
-//               memory; a per-digit prefix over warps makes the tile scatter
-//               stable. Keys are read twice (histogram + scatter) and written once.
+//               memory; a per-digit prefix over warps makes the tile order
+//               stable; the tile is placed digit-sorted in shared memory and
+//               written out run by run (coalesced). Keys are read twice
+//               (histogram + scatter) and written once.
 #include "common.cuh"
 #include "sort.cuh"
 
