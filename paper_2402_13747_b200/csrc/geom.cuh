@@ -161,6 +161,9 @@ static __device__ __noinline__ SurfaceEstimate estimate_surface(const V3& x, uin
   double best_d2 = 1.7976931348623157e308;
   const uint2 r = g.ie_range[ie];
   uint32_t best = r.x;
+  // unrolled: consecutive points' exp() chains are independent and overlap; the sums
+  // still run in point order
+#pragma unroll 4
   for (uint32_t i = r.x; i < r.y; ++i) {
     const uint32_t pi = g.point_indices[i];
     const V3 p = load3(s.pos + 3ull * pi);
