@@ -350,6 +350,8 @@ def b200_arm(args, rank, world, local_rank):
                                        f"rows all-gathered over {args.backend.upper()}" if world > 1 else "single GPU"),
                        "l2": "flushed (256 MB write) before every timed step"},
             "rays_per_step": rays, "exact_paths_per_s": exact_per_s, "candidates_refined_per_s": cand_per_s,
+            # Mrays/s over the trace stage alone (R / t_trace), beside `value` (R / step)
+            "mrays_per_s_trace": rays / dict(s0["timings"]).get("trace", float("nan")) / 1e6,
             "exact_paths": s0["exact_paths"], "coarse_paths": s0["coarse_paths"],
             "stage_seconds": dict(s0["timings"]), "kernel_share": shares,
             "roofline": rl,
