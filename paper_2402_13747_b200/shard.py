@@ -58,6 +58,31 @@ def all_gather_bytes(buf: torch.Tensor, group=None) -> torch.Tensor:
     return torch.cat([out[r * cap: r * cap + sizes[r]] for r in range(world)])
 
 
+def gather_bytes(buf: torch.Tensor, dst: int = 0, group=None):
+    """Concatenation in rank order of every rank's 1-D uint8 tensor on rank `dst` (None
+    elsewhere): only the destination receives the bytes (the outcome rows go to the
+    one rank that finishes)."""
+    if buf.is_cuda and dist.get_backend(group) == "gloo":
+        out = gather_bytes(buf.cpu(), dst, group)
+        return None if out is None else out.to(buf.device)
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    dev = buf.device
+    size = torch.tensor([buf.numel()], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros_like(size) for _ in range(world)]
+    dist.all_gather(sizes, size, group=group)
+    sizes = [int(x.item()) for x in sizes]
+    cap = max(sizes) if sizes else 0
+    if cap == 0:
+        return torch.empty(0, dtype=torch.uint8, device=dev) if rank == dst else None
+    padded = torch.zeros(cap, dtype=torch.uint8, device=dev)
+    padded[: buf.numel()] = buf
+    parts = [torch.empty(cap, dtype=torch.uint8, device=dev) for _ in range(world)] if rank == dst else None
+    dist.gather(padded, parts, dst=dst, group=group)
+    if rank != dst:
+        return None
+    return torch.cat([parts[r][: sizes[r]] for r in range(world)])
+
+
 def sum_stats(stats: np.ndarray, group=None, device=None) -> np.ndarray:
     """Element-wise sum of every rank's pcr_shard_stats counters."""
     if dist.get_backend(group) == "gloo":
@@ -89,7 +114,7 @@ def run_pipeline_sharded(scene: pcray.DeviceScene, config: abi.RunConfig | None 
     if n_out:
         pcray.shard_outcomes(ctx, outs.data_ptr())
     totals = sum_stats(pcray.shard_stats(ctx), group, dev)
-    all_outs = all_gather_bytes(outs, group)
+    all_outs = gather_bytes(outs, 0, group)
     torch.cuda.current_stream().synchronize()
     if rank != 0:
         return None

@@ -65,7 +65,8 @@ def _worker(rank, world, port, q):
         got = shard.all_gather_bytes(buf)
         empty = shard.all_gather_bytes(torch.empty(0, dtype=torch.uint8))
         st = shard.sum_stats(np.arange(7, dtype=np.uint64) * (rank + 1))
-        q.put((rank, got.tolist(), empty.numel(), st.tolist()))
+        g0 = shard.gather_bytes(buf, 0)
+        q.put((rank, got.tolist(), empty.numel(), st.tolist(), None if g0 is None else g0.tolist()))
     finally:
         dist.destroy_process_group()
 
@@ -85,7 +86,8 @@ def test_exchange_gloo(world):
     sizes = [5, 0, 13][:world]
     want = [r + 1 for r in range(world) for _ in range(sizes[r])]
     tot = sum(range(1, world + 1))
-    for rank, got, empty, st in res:
+    for rank, got, empty, st, g0 in res:
         assert got == want, rank
         assert empty == 0
         assert st == [i * tot for i in range(7)]
+        assert g0 == (want if rank == 0 else None)
