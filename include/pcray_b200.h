@@ -306,6 +306,37 @@ int pcr_scene_points(pcr_ctx* ctx, const pcr_scene* scene, double* position, dou
  * to the reference's for the same paths and config hash. */
 int pcr_write_paths(pcr_ctx* ctx, const char* path, const pcr_paths* paths, uint64_t config_hash);
 
+/* Diffraction edges of an edges file, host-side (the layout pcr_scene_desc takes). */
+typedef struct pcr_edges {
+  uint32_t n;
+  double* geometry; /* n*12: start, end, normal_a, normal_b (normals unit length) */
+  uint32_t* label;  /* n */
+} pcr_edges;
+/* load_edges (io.hpp:19-21; io.cpp:191-229): 13 whitespace-separated numbers per record
+ * (start xyz, end xyz, normal_a xyz, normal_b xyz, label), '#' starts a comment, blank
+ * lines skipped; normals normalised on load. Errors: "cannot open edges file: <path>",
+ * "edge record R: expected 13 values" / "degenerate edge" / "zero normal" / "normal not
+ * perpendicular to edge". */
+int pcr_load_edges(pcr_ctx* ctx, const char* path, pcr_edges** out);
+void pcr_free_edges(pcr_edges* edges);
+
+/* The file-level fields of RunConfig (pipeline.hpp:12-32) that run_pipeline_on_scene
+ * does not take. NULL or "" means "not given", as the reference's empty strings. */
+typedef struct pcr_run_files {
+  const char* scene_path;  /* PLY point cloud */
+  const char* edges_path;  /* edges file */
+  const char* output_path; /* paths JSONL */
+  const double* tx_position; /* n_tx*3; ids assigned 0..n_tx-1 in order */
+  uint32_t n_tx;
+  const double* rx_position; /* n_rx*3; ids 0..n_rx-1 */
+  uint32_t n_rx;
+} pcr_run_files;
+/* run_pipeline (pipeline.hpp:63-64; pipeline.cpp:214-247): load (PLY straight to the
+ * device + edges) -> run_pipeline_on_scene -> write the paths JSONL when output_path is
+ * given. Timings gain "load" first and "write" last; load and write failures carry the
+ * "load: " / "write: " prefixes. */
+int pcr_run_pipeline(pcr_ctx* ctx, const pcr_run_files* files, const pcr_run_config* config, pcr_summary** out);
+
 /* ---- sharded pipeline: one process per GPU ----------------------------- */
 /* run_pipeline_on_scene split across n_shards contexts (one per GPU). The reference
  * parallelises the same loop over initial hits (tracer.cpp:476-533, parallel_for) and

@@ -119,6 +119,8 @@ def _load(path):
                                               pp(pp(C.c_uint32)), pp(C.c_uint64)]
         L.pcrref_free.argtypes = [vp]
         L.pcrref_write_paths.argtypes = [C.c_char_p, pp(abi.Paths), C.c_uint64]
+        L.pcrref_load_edges.argtypes = [C.c_char_p, pp(pp(abi.Edges))]
+        L.pcrref_run_pipeline.argtypes = [pp(abi.RunFiles), pp(abi.RunConfig), pp(pp(abi.Summary))]
         _libs[path] = L
     return _libs[path]
 
@@ -339,3 +341,29 @@ def write_paths(path: str, paths: dict, config_hash: int) -> None:
     """pcray::write_paths (io.hpp:33-34)."""
     keep = abi.PathsKeepAlive(paths)
     _check(lib().pcrref_write_paths(path.encode(), C.byref(keep.paths), config_hash))
+
+
+def load_edges(path: str) -> dict:
+    """pcray::load_edges (io.hpp:19-21) -> {start, end, normal_a, normal_b, label}."""
+    out = C.POINTER(abi.Edges)()
+    _check(lib().pcrref_load_edges(path.encode(), C.byref(out)))
+    try:
+        return abi.edges_to_dict(out.contents)
+    finally:
+        e = out.contents
+        lib().pcrref_free(C.cast(e.geometry, C.c_void_p))
+        lib().pcrref_free(C.cast(e.label, C.c_void_p))
+        lib().pcrref_free(C.cast(out, C.c_void_p))
+
+
+def run_pipeline(scene_path: str = "", edges_path: str = "", output_path: str = "", transmitters=(),
+                 receivers=(), config: abi.RunConfig | None = None) -> dict:
+    """pcray::run_pipeline (pipeline.hpp:63-64): files in, RunSummary (+ JSONL) out."""
+    config = config or default_run_config()
+    keep = abi.RunFilesKeepAlive(scene_path, edges_path, output_path, transmitters, receivers)
+    out = C.POINTER(abi.Summary)()
+    _check(lib().pcrref_run_pipeline(C.byref(keep.files), C.byref(config), C.byref(out)))
+    try:
+        return abi.summary_to_dict(out.contents)
+    finally:
+        lib().pcrref_free_summary(out)

@@ -577,32 +577,66 @@ void pcrref_free_outcomes(pcr_outcomes* o) {
 }
 
 // ---- whole pipeline ----------------------------------------------------------------
+// RunSummary (pipeline.hpp:40-58) into the pcr_summary layout
+static pcr_summary* summary_of(const RunSummary& rs) {
+  pcr_summary* s = alloc<pcr_summary>(1);
+  s->point_count = rs.point_count;
+  s->edge_count = rs.edge_count;
+  s->ie_count = rs.ie_count;
+  for (int a = 0; a < 3; ++a) s->grid_dims[a] = rs.grid_dims[a];
+  s->coarse_paths = rs.coarse_paths;
+  s->refined_paths = rs.refined_paths;
+  for (int r = 0; r < 4; ++r) s->rejected[r] = rs.rejected[r];
+  s->exact_paths = rs.exact_paths;
+  s->n_timings = static_cast<std::uint32_t>(std::min<std::size_t>(rs.timings.size(), PCR_MAX_STAGES));
+  for (std::uint32_t t = 0; t < s->n_timings; ++t) {
+    std::snprintf(s->timing_stage[t], sizeof(s->timing_stage[t]), "%s", rs.timings[t].stage.c_str());
+    s->timing_seconds[t] = rs.timings[t].seconds;
+  }
+  s->hash = rs.hash;
+  std::size_t stride = 1;
+  for (const auto& p : rs.paths) stride = std::max(stride, p.interactions.size());
+  pcr_paths* pp = alloc_paths(rs.paths.size(), static_cast<std::uint32_t>(stride));
+  for (std::size_t i = 0; i < rs.paths.size(); ++i) put_exact(pp, i, rs.paths[i]);
+  s->paths = *pp;
+  std::free(pp);
+  return s;
+}
+
 // run_pipeline_on_scene (pipeline.cpp:99-212)
 int pcrref_run_pipeline_on_scene(const void* scene, const pcr_run_config* cfg, pcr_summary** out) {
+  return guarded([&] { *out = summary_of(run_pipeline_on_scene(*static_cast<const Scene*>(scene), run_config(cfg))); });
+}
+
+// run_pipeline (pipeline.hpp:63-64): the file-level run, paths and radios from `files`
+int pcrref_run_pipeline(const pcr_run_files* f, const pcr_run_config* cfg, pcr_summary** out) {
   return guarded([&] {
-    const RunSummary rs = run_pipeline_on_scene(*static_cast<const Scene*>(scene), run_config(cfg));
-    pcr_summary* s = alloc<pcr_summary>(1);
-    s->point_count = rs.point_count;
-    s->edge_count = rs.edge_count;
-    s->ie_count = rs.ie_count;
-    for (int a = 0; a < 3; ++a) s->grid_dims[a] = rs.grid_dims[a];
-    s->coarse_paths = rs.coarse_paths;
-    s->refined_paths = rs.refined_paths;
-    for (int r = 0; r < 4; ++r) s->rejected[r] = rs.rejected[r];
-    s->exact_paths = rs.exact_paths;
-    s->n_timings = static_cast<std::uint32_t>(std::min<std::size_t>(rs.timings.size(), PCR_MAX_STAGES));
-    for (std::uint32_t t = 0; t < s->n_timings; ++t) {
-      std::snprintf(s->timing_stage[t], sizeof(s->timing_stage[t]), "%s", rs.timings[t].stage.c_str());
-      s->timing_seconds[t] = rs.timings[t].seconds;
+    RunConfig rc = run_config(cfg);
+    if (f->scene_path) rc.scene_path = f->scene_path;
+    if (f->edges_path) rc.edges_path = f->edges_path;
+    if (f->output_path) rc.output_path = f->output_path;
+    for (std::uint32_t i = 0; i < f->n_tx; ++i) rc.transmitters.push_back(get3(f->tx_position + 3 * i));
+    for (std::uint32_t i = 0; i < f->n_rx; ++i) rc.receivers.push_back(get3(f->rx_position + 3 * i));
+    *out = summary_of(run_pipeline(rc));
+  });
+}
+
+// load_edges (io.hpp:19-21) into the pcr_edges layout
+int pcrref_load_edges(const char* path, pcr_edges** out) {
+  return guarded([&] {
+    const auto edges = load_edges(path);
+    pcr_edges* e = alloc<pcr_edges>(1);
+    e->n = static_cast<std::uint32_t>(edges.size());
+    e->geometry = alloc<double>(12 * edges.size() + 1);
+    e->label = alloc<std::uint32_t>(edges.size() + 1);
+    for (std::size_t i = 0; i < edges.size(); ++i) {
+      put3(e->geometry + 12 * i, edges[i].start);
+      put3(e->geometry + 12 * i + 3, edges[i].end);
+      put3(e->geometry + 12 * i + 6, edges[i].normal_a);
+      put3(e->geometry + 12 * i + 9, edges[i].normal_b);
+      e->label[i] = edges[i].label;
     }
-    s->hash = rs.hash;
-    std::size_t stride = 1;
-    for (const auto& p : rs.paths) stride = std::max(stride, p.interactions.size());
-    pcr_paths* pp = alloc_paths(rs.paths.size(), static_cast<std::uint32_t>(stride));
-    for (std::size_t i = 0; i < rs.paths.size(); ++i) put_exact(pp, i, rs.paths[i]);
-    s->paths = *pp;
-    std::free(pp);
-    *out = s;
+    *out = e;
   });
 }
 

@@ -6,6 +6,7 @@ Only struct layouts and numpy<->struct conversion live here; the loaders are in
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -102,6 +103,37 @@ class Summary(C.Structure):
         ("refine_trials", C.c_uint64), ("refine_marches", C.c_uint64), ("walk_cells", C.c_uint64),
         ("walk_ies", C.c_uint64),
     ]
+
+
+class Edges(C.Structure):
+    """pcr_edges: an edges file on the host (geometry n*12: start, end, normal_a, normal_b)."""
+    _fields_ = [("n", C.c_uint32), ("geometry", C.POINTER(C.c_double)), ("label", C.POINTER(C.c_uint32))]
+
+
+def edges_to_dict(e: Edges) -> dict:
+    n = int(e.n)
+    g = np.ctypeslib.as_array(e.geometry, (12 * n + 1,))[: 12 * n].reshape(n, 12).copy()
+    return {"start": g[:, 0:3], "end": g[:, 3:6], "normal_a": g[:, 6:9], "normal_b": g[:, 9:12],
+            "label": np.ctypeslib.as_array(e.label, (n + 1,))[:n].copy()}
+
+
+class RunFiles(C.Structure):
+    """pcr_run_files: RunConfig's file paths and radio lists (pipeline.hpp:12-32)."""
+    _fields_ = [("scene_path", C.c_char_p), ("edges_path", C.c_char_p), ("output_path", C.c_char_p),
+                ("tx_position", C.POINTER(C.c_double)), ("n_tx", C.c_uint32),
+                ("rx_position", C.POINTER(C.c_double)), ("n_rx", C.c_uint32)]
+
+
+class RunFilesKeepAlive:
+    """A RunFiles plus the arrays its pointers reference."""
+
+    def __init__(self, scene_path="", edges_path="", output_path="", transmitters=(), receivers=()):
+        enc = lambda p: os.fsencode(p) if p else b""  # noqa: E731
+        self.tx = np.ascontiguousarray(np.asarray(transmitters, dtype=np.float64).reshape(-1, 3))
+        self.rx = np.ascontiguousarray(np.asarray(receivers, dtype=np.float64).reshape(-1, 3))
+        self.files = RunFiles(enc(scene_path), enc(edges_path), enc(output_path),
+                              self.tx.ctypes.data_as(C.POINTER(C.c_double)), len(self.tx),
+                              self.rx.ctypes.data_as(C.POINTER(C.c_double)), len(self.rx))
 
 
 SHARD_STATS_FIELDS = ("cone_traces", "visibility_tests", "walk_cells", "walk_ies", "refine_iterations",

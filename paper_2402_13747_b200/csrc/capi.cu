@@ -377,6 +377,38 @@ int pcr_write_paths(pcr_ctx* ctx, const char* path, const pcr_paths* paths, uint
   });
 }
 
+int pcr_load_edges(pcr_ctx* ctx, const char* path, pcr_edges** out) {
+  return guarded(ctx, [&] {
+    if (!path || !out) throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    std::vector<double> g;
+    std::vector<uint32_t> l;
+    pcr::api_load_edges(path, g, l);
+    pcr_edges* e = pcr::halloc<pcr_edges>(1);
+    e->n = static_cast<uint32_t>(l.size());
+    e->geometry = pcr::halloc<double>(g.size() + 1);
+    e->label = pcr::halloc<uint32_t>(l.size() + 1);
+    if (!g.empty()) std::memcpy(e->geometry, g.data(), g.size() * sizeof(double));
+    if (!l.empty()) std::memcpy(e->label, l.data(), l.size() * sizeof(uint32_t));
+    *out = e;
+  });
+}
+
+void pcr_free_edges(pcr_edges* e) {
+  if (!e) return;
+  std::free(e->geometry);
+  std::free(e->label);
+  std::free(e);
+}
+
+int pcr_run_pipeline(pcr_ctx* ctx, const pcr_run_files* files, const pcr_run_config* config, pcr_summary** out) {
+  return guarded(ctx, [&] {
+    if (!files || !config || !out) throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    if ((files->n_tx && !files->tx_position) || (files->n_rx && !files->rx_position))
+      throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    pcr::api_run_pipeline(ctx->c, *files, *config, out);
+  });
+}
+
 int pcr_shard_trace(pcr_ctx* ctx, const pcr_scene* scene, const pcr_run_config* config, uint32_t shard,
                     uint32_t n_shards, uint64_t* n_rows, uint64_t* row_bytes) {
   return guarded(ctx, [&] {

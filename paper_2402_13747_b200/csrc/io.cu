@@ -9,7 +9,12 @@
 //   ascii data is parsed on the host as the reference does (istream >> double).
 // * the paths JSONL writer (write_paths, proj/src/io.cpp:317-349): same header line,
 //   same field order, %.9g numbers, records in the order given.
+// * the edges file (load_edges, proj/src/io.cpp:191-229) and the file-level pipeline
+//   run (run_pipeline, proj/src/pipeline.cpp:214-247) that ties the three together.
 #include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
 
 #include <cerrno>
 #include <cstdio>
@@ -307,6 +312,144 @@ void api_write_paths(const char* path, const pcr_paths& p, uint64_t config_hash)
   }
   out.write(buf.data(), static_cast<std::streamsize>(buf.size()));
   if (!out) throw Error(PCR_ERR_RUNTIME, std::string("write failure: ") + path);
+}
+
+namespace {
+
+double sq3(const double* v) { return (v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]; }
+
+}  // namespace
+
+// load_edges (io.cpp:191-229): records are parsed with istream >> double like the
+// reference (same grammar, same rounding, same failure points); per record the edge
+// must be non-degenerate (|end - start| >= 1e-12), both normals non-zero, and after
+// normalisation (v / sqrt(v.v), Eigen's normalize) perpendicular to the edge direction
+// within 1e-3.
+void api_load_edges(const char* path, std::vector<double>& geom, std::vector<uint32_t>& label) {
+  std::ifstream in(path);
+  if (!in) throw Error(PCR_ERR_RUNTIME, std::string("cannot open edges file: ") + path);
+  geom.clear();
+  label.clear();
+  std::string line;
+  size_t record = 0;
+  auto fail = [&](const char* what) {
+    throw Error(PCR_ERR_RUNTIME, "edge record " + std::to_string(record) + ": " + what);
+  };
+  while (std::getline(in, line)) {
+    const size_t hash = line.find('#');
+    if (hash != std::string::npos) line.erase(hash);
+    std::istringstream iss(line);
+    double v[13];
+    if (!(iss >> v[0])) continue;  // blank or comment-only line
+    for (int i = 1; i < 13; ++i)
+      if (!(iss >> v[i])) fail("expected 13 values");
+    double d[3] = {v[3] - v[0], v[4] - v[1], v[5] - v[2]};
+    if (std::sqrt(sq3(d)) < 1e-12) fail("degenerate edge");
+    double* na = v + 6;
+    double* nb = v + 9;
+    if (std::sqrt(sq3(na)) < 1e-12 || std::sqrt(sq3(nb)) < 1e-12) fail("zero normal");
+    for (double* n : {na, nb}) {
+      const double z = sq3(n);
+      if (z > 0) {
+        const double r = std::sqrt(z);
+        for (int a = 0; a < 3; ++a) n[a] /= r;
+      }
+    }
+    const double dz = sq3(d);
+    if (dz > 0) {
+      const double r = std::sqrt(dz);
+      for (int a = 0; a < 3; ++a) d[a] /= r;
+    }
+    const double wa = (d[0] * na[0] + d[1] * na[1]) + d[2] * na[2];
+    const double wb = (d[0] * nb[0] + d[1] * nb[1]) + d[2] * nb[2];
+    if (std::abs(wa) > 1e-3 || std::abs(wb) > 1e-3) fail("normal not perpendicular to edge");
+    geom.insert(geom.end(), v, v + 12);
+    label.push_back(static_cast<uint32_t>(v[12]));
+    ++record;
+  }
+}
+
+// run_pipeline (pipeline.cpp:214-247). The point cloud goes straight to the device
+// (api_scene_load_ply); radios get ids 0..n-1 in the order given; the "load" timing
+// (points, edges, radios) is inserted before the pipeline's own stages and "write"
+// appended after the JSONL is written.
+void api_run_pipeline(Ctx& ctx, const pcr_run_files& f, const pcr_run_config& cfg, pcr_summary** out) {
+  using Clock = std::chrono::steady_clock;
+  auto since = [](Clock::time_point t) { return std::chrono::duration<double>(Clock::now() - t).count(); };
+  const bool has_scene = f.scene_path && *f.scene_path;
+  const bool has_edges = f.edges_path && *f.edges_path;
+  const bool has_output = f.output_path && *f.output_path;
+  auto t0 = Clock::now();
+  SceneDev S;
+  std::vector<double> eg;
+  std::vector<uint32_t> el;
+  std::vector<uint32_t> tx_id(f.n_tx), rx_id(f.n_rx);
+  for (uint32_t i = 0; i < f.n_tx; ++i) tx_id[i] = i;
+  for (uint32_t i = 0; i < f.n_rx; ++i) rx_id[i] = i;
+  pcr_scene_desc rest{};
+  rest.carrier_frequency_hz = cfg.carrier_frequency_hz;
+  try {
+    if (has_scene) {
+      api_scene_load_ply(ctx, f.scene_path, rest, S);
+    } else {
+      S.n_points = 0;
+      S.pos.alloc(3, ctx.stream);
+      S.nrm.alloc(3, ctx.stream);
+      S.label.alloc(1, ctx.stream);
+    }
+    if (has_edges) api_load_edges(f.edges_path, eg, el);
+  } catch (const std::exception& e) {
+    const Error* pe = dynamic_cast<const Error*>(&e);
+    throw Error(pe ? pe->code : PCR_ERR_RUNTIME, std::string("load: ") + e.what());
+  }
+  rest.edge_geometry = eg.data();
+  rest.edge_label = el.data();
+  rest.n_edges = static_cast<uint32_t>(el.size());
+  rest.tx_position = f.tx_position;
+  rest.tx_id = tx_id.data();
+  rest.n_tx = f.n_tx;
+  rest.rx_position = f.rx_position;
+  rest.rx_id = rx_id.data();
+  rest.n_rx = f.n_rx;
+  upload_rest(ctx, rest, S);
+  PCR_CUDA(cudaStreamSynchronize(ctx.stream));
+  const double load_seconds = since(t0);
+
+  pcr_summary* sum = nullptr;
+  api_run_pipeline_device(ctx, S, cfg, &sum);
+  struct Guard {
+    pcr_summary* s;
+    ~Guard() {
+      if (s) {
+        free_paths_arrays(&s->paths);
+        std::free(s);
+      }
+    }
+  } guard{sum};
+  if (sum->n_timings < PCR_MAX_STAGES) {
+    for (uint32_t t = sum->n_timings; t > 0; --t) {
+      std::memcpy(sum->timing_stage[t], sum->timing_stage[t - 1], sizeof(sum->timing_stage[t]));
+      sum->timing_seconds[t] = sum->timing_seconds[t - 1];
+    }
+    std::snprintf(sum->timing_stage[0], sizeof(sum->timing_stage[0]), "load");
+    sum->timing_seconds[0] = load_seconds;
+    ++sum->n_timings;
+  }
+  if (has_output) {
+    t0 = Clock::now();
+    try {
+      api_write_paths(f.output_path, sum->paths, sum->hash);
+    } catch (const std::exception& e) {
+      const Error* pe = dynamic_cast<const Error*>(&e);
+      throw Error(pe ? pe->code : PCR_ERR_RUNTIME, std::string("write: ") + e.what());
+    }
+    if (sum->n_timings < PCR_MAX_STAGES) {
+      std::snprintf(sum->timing_stage[sum->n_timings], sizeof(sum->timing_stage[0]), "write");
+      sum->timing_seconds[sum->n_timings++] = since(t0);
+    }
+  }
+  *out = sum;
+  guard.s = nullptr;
 }
 
 }  // namespace pcr

@@ -25,6 +25,8 @@ void api_run_pipeline_device(Ctx& ctx, const SceneDev& scene, const pcr_run_conf
 void api_scene_load_ply(Ctx& ctx, const char* path, const pcr_scene_desc& rest, SceneDev& S);
 void api_scene_points(Ctx& ctx, const SceneDev& S, double* pos, double* nrm, uint32_t* label);
 void api_write_paths(const char* path, const pcr_paths& p, uint64_t config_hash);
+void api_load_edges(const char* path, std::vector<double>& geom, std::vector<uint32_t>& label);
+void api_run_pipeline(Ctx& ctx, const pcr_run_files& f, const pcr_run_config& cfg, pcr_summary** out);
 // sharded pipeline (pipeline.cu)
 void api_shard_trace(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, uint32_t shard, uint32_t n_shards,
                      uint64_t* n_rows, uint64_t* row_bytes);

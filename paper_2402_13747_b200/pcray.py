@@ -66,6 +66,10 @@ def lib():
         L.pcr_scene_load_ply.argtypes = [vp, C.c_char_p, pp(abi.SceneDesc), pp(vp)]
         L.pcr_scene_points.argtypes = [vp, vp, pp(C.c_double), pp(C.c_double), pp(C.c_uint32), pp(C.c_uint64)]
         L.pcr_write_paths.argtypes = [vp, C.c_char_p, pp(abi.Paths), C.c_uint64]
+        L.pcr_load_edges.argtypes = [vp, C.c_char_p, pp(pp(abi.Edges))]
+        L.pcr_free_edges.argtypes = [pp(abi.Edges)]
+        L.pcr_free_edges.restype = None
+        L.pcr_run_pipeline.argtypes = [vp, pp(abi.RunFiles), pp(abi.RunConfig), pp(pp(abi.Summary))]
         L.pcr_shard_trace.argtypes = [vp, vp, pp(abi.RunConfig), C.c_uint32, C.c_uint32, pp(C.c_uint64),
                                       pp(C.c_uint64)]
         L.pcr_shard_rows.argtypes = [vp, vp]
@@ -101,7 +105,8 @@ EXPORTED_SYMBOLS = [
     "pcr_run_config_defaults", "pcr_free_paths", "pcr_free_initial_hits", "pcr_free_outcomes",
     "pcr_free_summary", "pcr_free_receptions", "pcr_run_pipeline_device", "pcr_shard_trace", "pcr_shard_rows",
     "pcr_shard_refine", "pcr_shard_outcomes", "pcr_shard_stats_get", "pcr_shard_finish", "pcr_scene_load_ply",
-    "pcr_scene_points", "pcr_write_paths", "pcr_libm_exp_batch",
+    "pcr_scene_points", "pcr_write_paths", "pcr_libm_exp_batch", "pcr_load_edges", "pcr_free_edges",
+    "pcr_run_pipeline",
 ]
 
 
@@ -353,6 +358,31 @@ def write_paths(path: str, paths: dict, config_hash: int, ctx: Context | None = 
     ctx = ctx or Context.default()
     keep = abi.PathsKeepAlive(paths)
     ctx.check(lib().pcr_write_paths(ctx.handle, os.fsencode(path), C.byref(keep.paths), config_hash))
+
+
+def load_edges(path: str, ctx: Context | None = None) -> dict:
+    """pcray::load_edges (io.hpp:19-21) -> {start, end, normal_a, normal_b, label}."""
+    ctx = ctx or Context.default()
+    out = C.POINTER(abi.Edges)()
+    ctx.check(lib().pcr_load_edges(ctx.handle, os.fsencode(path), C.byref(out)))
+    try:
+        return abi.edges_to_dict(out.contents)
+    finally:
+        lib().pcr_free_edges(out)
+
+
+def run_pipeline(scene_path: str = "", edges_path: str = "", output_path: str = "", transmitters=(),
+                 receivers=(), config: RunConfig | None = None, ctx: Context | None = None) -> dict:
+    """pcray::run_pipeline (pipeline.hpp:63-64): files in, RunSummary (+ JSONL) out."""
+    ctx = ctx or Context.default()
+    config = config or default_run_config()
+    keep = abi.RunFilesKeepAlive(scene_path, edges_path, output_path, transmitters, receivers)
+    out = C.POINTER(abi.Summary)()
+    ctx.check(lib().pcr_run_pipeline(ctx.handle, C.byref(keep.files), C.byref(config), C.byref(out)))
+    try:
+        return abi.summary_to_dict(out.contents)
+    finally:
+        lib().pcr_free_summary(out)
 
 
 # ---- sharded pipeline (one process per GPU; orchestration in shard.py) ---------------------------

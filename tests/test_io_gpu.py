@@ -165,3 +165,107 @@ def test_paths_jsonl_byte_identical(oracle, gpu, tmp_path, name, mi, md):
 def test_write_paths_error(gpu, tmp_path):
     with pytest.raises(pcray.PcrError, match="cannot write paths file"):
         pcray.write_paths(str(tmp_path / "no_such_dir" / "x.jsonl"), {"n": 0, "stride": 1}, 0)
+
+
+# ---- edges file + file-level run_pipeline (io.cpp:191-229, pipeline.cpp:214-247) -------------------
+def _save_edges(path, scene):
+    with open(path, "w") as f:
+        f.write("# start_xyz end_xyz normal_a_xyz normal_b_xyz label\n")
+        for g, lab in zip(np.asarray(scene.edges).reshape(-1, 12), scene.edge_label):
+            f.write(" ".join(repr(float(v)) for v in g) + f" {int(lab)}\n")
+
+
+def _edges_equal(got, ref):
+    for k in ["start", "end", "normal_a", "normal_b", "label"]:
+        a, b = np.ascontiguousarray(got[k]), np.ascontiguousarray(ref[k])
+        assert a.shape == b.shape, k
+        if a.dtype == np.float64:
+            a, b = a.view(np.uint64), b.view(np.uint64)
+        assert np.array_equal(a, b), k
+
+
+def test_load_edges_parity(oracle, gpu, tmp_path):
+    f = tmp_path / "edges.txt"
+    f.write_text("# header comment\n"
+                 "\n"
+                 "   \t\n"
+                 "0 0 0 1 0 0 0 0 2 0 -3 0 7   # trailing comment\n"
+                 "-2e0 0 1 +2 0 1 0 -1.5 0 0 0 3e-1 7.9\n"
+                 "0.1 0.2 0.3 0.1 0.2 3.3 1 1e-5 0 -0.70710678118654757 0.7071067811865476 0 4294967295\n"
+                 "not-a-number line is skipped like a blank one\n"
+                 "1 2 3 1 2 4 0.6 0.8 0 0 1e300 0 12 extra tokens ignored\n")
+    ref = oracle.load_edges(str(f))
+    got = pcray.load_edges(str(f))
+    assert len(ref["label"]) == 4
+    _edges_equal(got, ref)
+    # C2's own edges through a file
+    scene, _ = scenes.build_scene("C2")
+    g = str(tmp_path / "c2_edges.txt")
+    _save_edges(g, scene)
+    _edges_equal(pcray.load_edges(g), oracle.load_edges(g))
+
+
+@pytest.mark.parametrize("text", [
+    "0 0 0 0 0 0 0 0 1 0 -1 0 7\n",
+    "0 0 0 1 0 0 0 0 1 0 -1 0\n",
+    "0 0 0 1 0 0 1 0 0 0 -1 0 7\n",
+    "0 0 0 1 0 0 0 0 0 0 -1 0 7\n",
+    "0 0 0 1 0 0 0 0 1 0 -1 0 7\n0 0 0 1 0 0 0 0 1 0 -1 x 7\n",
+    "0 0 0 1 0 0 0 0 1 0 1e-12 0 7\n# c\n0 0 0 1 0 0 0 0 1 0.002 1 0 3\n",
+    "0 0 0 1 0 0 0 0 1 0 -1 0 7\n0 0 0 1e-13 0 0 0 0 1 0 -1 0 7\n",
+])
+def test_load_edges_error_texts(oracle, gpu, tmp_path, text):
+    f = tmp_path / "bad.txt"
+    f.write_text(text)
+    with pytest.raises(oracle.RefError) as r:
+        oracle.load_edges(str(f))
+    with pytest.raises(pcray.PcrError) as g:
+        pcray.load_edges(str(f))
+    assert str(g.value) == str(r.value)
+    missing = str(tmp_path / "nope.txt")
+    with pytest.raises(pcray.PcrError, match="cannot open edges file: " + missing):
+        pcray.load_edges(missing)
+
+
+@pytest.mark.parametrize("binary", [True, False])
+def test_run_pipeline_files_c2(oracle, gpu, tmp_path, binary):
+    scene, _ = scenes.build_scene("C2")
+    ply, edges = str(tmp_path / "c2.ply"), str(tmp_path / "c2_edges.txt")
+    oracle.save_point_cloud(ply, oracle.RefScene(scene), binary)
+    _save_edges(edges, scene)
+    kw = dict(max_interactions=2, max_diffractions=1)
+    a, b = str(tmp_path / "gpu.jsonl"), str(tmp_path / "ref.jsonl")
+    ref = oracle.run_pipeline(ply, edges, b, scene.tx, scene.rx, oracle.default_run_config(**kw))
+    got = pcray.run_pipeline(ply, edges, a, scene.tx, scene.rx, abi.default_run_config(**kw))
+    for k in ["point_count", "edge_count", "ie_count", "coarse_paths", "refined_paths", "exact_paths", "hash"]:
+        assert got[k] == ref[k], k
+    assert list(got["rejected"]) == list(ref["rejected"])
+    assert [t[0] for t in got["timings"]] == [t[0] for t in ref["timings"]]
+    assert got["timings"][0][0] == "load" and got["timings"][-1][0] == "write"
+    assert got["exact_paths"] > 0
+    assert open(a, "rb").read() == open(b, "rb").read()
+
+
+def test_run_pipeline_files_error_texts(oracle, gpu, tmp_path):
+    scene, _ = scenes.build_scene("C1")
+    ply = str(tmp_path / "c1.ply")
+    oracle.save_point_cloud(ply, oracle.RefScene(scene), True)
+    bad_edges = tmp_path / "bad.txt"
+    bad_edges.write_text("0 0 0 1 0 0 1 0 0 0 -1 0 7\n")
+    cases = [
+        dict(scene_path=str(tmp_path / "nope.ply")),
+        dict(scene_path=str(tmp_path / "nope.ply"), edges_path=str(bad_edges)),  # points fail first
+        dict(scene_path=ply, edges_path=str(bad_edges)),
+        dict(scene_path=ply, edges_path=str(tmp_path / "nope.txt")),
+        dict(scene_path=ply, output_path=str(tmp_path / "no_dir" / "p.jsonl"), transmitters=scene.tx,
+             receivers=scene.rx),
+        dict(),  # nothing at all: validate
+        dict(scene_path=ply),  # no radios: validate
+    ]
+    cfg = dict(max_interactions=1)
+    for kw in cases:
+        with pytest.raises(oracle.RefError) as r:
+            oracle.run_pipeline(config=oracle.default_run_config(**cfg), **kw)
+        with pytest.raises(pcray.PcrError) as g:
+            pcray.run_pipeline(config=abi.default_run_config(**cfg), **kw)
+        assert str(g.value) == str(r.value), kw
