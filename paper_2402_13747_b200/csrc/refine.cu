@@ -120,8 +120,9 @@ __device__ __forceinline__ bool planar_candidate(const V3& prev, const V3& dir, 
 }
 
 // reproject (refine.cpp:80-130) with surface_ies_near (:34-52) scanned in place.
+// first_pass = 1 skips the same-label pass (done cooperatively by refine_warp_kernel).
 __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, const GridView& g, const SceneView& s,
-                          Reproj& out, uint32_t& n_march) {
+                          Reproj& out, uint32_t& n_march, int first_pass = 0) {
   const V3 diff = predicted - prev;
   const double dist = norm(diff);
   if (dist < kTiny) return false;
@@ -148,7 +149,7 @@ __device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, c
     nb_end = g.nb_off[c + 1];
   }
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
-  for (int pass = 0; pass < 2; ++pass) {
+  for (int pass = first_pass; pass < 2; ++pass) {
     const bool same = pass == 0;
     uint32_t best_ie = kNoIe;
     double best_t = 1.7976931348623157e308;
@@ -574,6 +575,433 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
   o.has_path[k] = 1;
 }
 
+// ---- warp-cooperative refinement ----------------------------------------------------
+// Measured on C2 (PCR_REFINE_TRACE): the thread-per-path kernel empties its queue after
+// ~1/4 of its run and spends the rest draining the last paths (up to rho = 2000
+// iterations each) with most lanes idle. Here the 32 lanes of a warp iterate their own
+// paths in lockstep, and the same-label reprojection scan (the bulk of an iteration)
+// runs as one flat loop over the concatenated label runs of every lane reprojecting
+// the same node index: lanes without a path (queue empty) scan for the others. Each
+// record's hit distance is computed as in the serial scan; the winner per path is the
+// least distance, ties to the earliest record in scan order — what the serial strict-<
+// scan returns — found by a segmented (t, index) min over the round's lane segments.
+// The scan's pruning (t_lo / t* against the best so far) only ever skips records that
+// cannot win, so pruning against the best of earlier rounds changes nothing.
+
+struct ScanSlot {  // one per lane: the reprojection it posted and its best record so far
+  double prev[3], dir[3], pred[3];
+  double best_t;
+  uint32_t pre, j0, best_f, pad;
+};
+
+template <int D>
+struct PathState {
+  uint32_t k;
+  int d, iter, power, lam;
+  V3 tx, rx;
+  double f, gnorm;
+  RNode nd[D];
+  V3 pts[D];
+  Snapshot<D> saved, last[2];
+};
+
+constexpr uint32_t kNoRec = 0xffffffffu;
+constexpr unsigned kFull = 0xffffffffu;
+
+// make_path_state (refine.cpp:134-161); false when the path is done at once (LOS)
+template <int D>
+__device__ bool path_init(PathState<D>& st, uint32_t k, const CandIn& in, const SceneView& s, const RefOut& o) {
+  const int d = static_cast<int>(in.n_inter[k]);
+  st.k = k;
+  st.d = d;
+  st.tx = load3(in.tx + 3ull * k);
+  st.rx = load3(in.rx + 3ull * k);
+  o.has_path[k] = 0;
+  o.iters[k] = 0;
+  if (d == 0) {  // LOS passes through (pipeline.cpp:160-170)
+    o.has_path[k] = 1;
+    o.reason[k] = PCR_NOT_CONVERGED;
+    o.length[k] = in.coarse_length[k];
+    o.delay[k] = in.coarse_length[k] / kSpeedOfLight;
+    o.gnorm[k] = 0.0;
+    return false;
+  }
+  for (int q = 0; q < d; ++q) {
+    const size_t j = static_cast<size_t>(k) * in.stride + q;
+    RNode& x = st.nd[q];
+    x.kind = in.kind[j];
+    x.c = load3(in.pos + 3 * j);
+    x.label = in.label[j];
+    x.edge = in.edge[j];
+    x.p0 = 0.0;
+    x.p1 = 0.0;
+    if (x.kind == 0) {
+      x.n = load3(in.nrm + 3 * j);
+      local_frame(x.n, x.a, x.b);
+      x.lo = x.hi = 0.0;
+    } else {
+      const double* e = s.edges + 12ull * x.edge;
+      const V3 es = load3(e), ee = load3(e + 3);
+      x.a = normalized(ee - es);
+      x.lo = dot(es - x.c, x.a);
+      x.hi = dot(ee - x.c, x.a);
+      x.b = V3{0, 1, 0};
+      x.n = V3{0, 0, 1};
+    }
+  }
+  for (int q = 0; q < d; ++q) st.pts[q] = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
+  st.f = chain_len(st.tx, st.pts, d, st.rx);
+  st.gnorm = 0.0;
+  st.iter = 0;
+  take_snapshot(st.saved, st.nd, d);
+  st.last[0] = st.saved;
+  st.last[1] = st.saved;
+  st.power = 1;
+  st.lam = 0;
+  return true;
+}
+
+// converged: final per-segment visibility (refine.cpp:256-265) and the refined path
+template <int D>
+__device__ void path_converged(const PathState<D>& st, const CandIn& in, const GridView& g, const SceneView& s,
+                               const RefOut& o) {
+  const uint32_t k = st.k;
+  const int d = st.d;
+  V3 prev = st.tx;
+  for (int q = 0; q <= d; ++q) {
+    const V3 next = q < d ? st.pts[q] : st.rx;
+    if (!segment_visible(prev, next, kNoIe, g, s)) {
+      o.reason[k] = PCR_OCCLUDED;
+      return;
+    }
+    prev = next;
+  }
+  for (int q = 0; q < d; ++q) {
+    const size_t j = static_cast<size_t>(k) * in.stride + q;
+    store3(o.pos + 3 * j, st.pts[q]);
+    if (st.nd[q].kind == 0) {
+      store3(o.nrm + 3 * j, st.nd[q].n);
+      o.label[j] = st.nd[q].label;
+    }
+  }
+  const double total = chain_len(st.tx, st.pts, d, st.rx);
+  o.length[k] = total;
+  o.delay[k] = total / kSpeedOfLight;
+  o.gnorm[k] = st.gnorm;
+  o.reason[k] = PCR_NOT_CONVERGED;
+  o.has_path[k] = 1;
+}
+
+// One iteration up to the reprojection: rho bound, local_gradients (:167-187), the
+// convergence test, backtracking (:209-232). False when the path is finished.
+template <int D>
+__device__ bool path_step_a(PathState<D>& st, const CandIn& in, const GridView& g, const SceneView& s, double delta,
+                            int rho, double step_size, const RefOut& o, uint32_t& n_trials) {
+  const uint32_t k = st.k;
+  const int d = st.d;
+  if (st.iter >= rho) {
+    o.iters[k] = static_cast<uint32_t>(st.iter);
+    o.reason[k] = PCR_NOT_CONVERGED;
+    return false;
+  }
+  double gr[2 * D];
+  int ng = 0;
+  for (int q = 0; q < d; ++q) {
+    const V3 prev = q == 0 ? st.tx : st.pts[q - 1];
+    const V3 next = q + 1 == d ? st.rx : st.pts[q + 1];
+    const V3 dp = st.pts[q] - prev;
+    const V3 dn = st.pts[q] - next;
+    const double lp = norm(dp), ln = norm(dn);
+    if (lp < kTiny || ln < kTiny) {
+      o.reason[k] = PCR_DEGENERATE;
+      o.iters[k] = static_cast<uint32_t>(st.iter + 1);
+      return false;
+    }
+    const V3 e_sum = dp / lp + dn / ln;
+    gr[ng++] = dot(st.nd[q].a, e_sum);
+    if (st.nd[q].kind == 0) gr[ng++] = dot(st.nd[q].b, e_sum);
+  }
+  double gn = 0.0;
+  for (int q = 0; q < ng; ++q) gn += gr[q] * gr[q];
+  st.gnorm = sqrt(gn);
+  if (st.gnorm < delta) {
+    o.iters[k] = static_cast<uint32_t>(st.iter + 1);
+    path_converged(st, in, g, s, o);
+    return false;
+  }
+  double step = step_size;
+  double tp0[D], tp1[D];
+  for (int h = 0; h <= 8; ++h) {
+    int gi = 0;
+    V3 tpts[D];
+    for (int q = 0; q < d; ++q) {
+      if (st.nd[q].kind == 0) {
+        tp0[q] = st.nd[q].p0 - step * gr[gi++];
+        tp1[q] = st.nd[q].p1 - step * gr[gi++];
+      } else {
+        tp0[q] = sclamp(st.nd[q].p0 - step * gr[gi++], st.nd[q].lo, st.nd[q].hi);
+        tp1[q] = st.nd[q].p1;
+      }
+      tpts[q] = node_point(st.nd[q], tp0[q], tp1[q]);
+    }
+    ++n_trials;
+    if (chain_len(st.tx, tpts, d, st.rx) <= st.f + 1e-15) {
+      for (int q = 0; q < d; ++q) {
+        st.nd[q].p0 = tp0[q];
+        st.nd[q].p1 = tp1[q];
+      }
+      return true;
+    }
+    step *= 0.5;
+  }
+  // fixed point: every remaining iteration repeats this one (not_converged)
+  o.iters[k] = static_cast<uint32_t>(st.iter + 1);
+  o.reason[k] = PCR_NOT_CONVERGED;
+  return false;
+}
+
+// After the reprojection: new chain length, cycle checks (see Snapshot), next iteration.
+template <int D>
+__device__ bool path_step_c(PathState<D>& st, const RefOut& o) {
+  const int d = st.d;
+  for (int q = 0; q < d; ++q) st.pts[q] = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
+  st.f = chain_len(st.tx, st.pts, d, st.rx);
+  const int slot = st.iter & 1;
+  if (same_snapshot(st.last[slot ^ 1], st.nd, d) || same_snapshot(st.last[slot], st.nd, d) ||
+      same_snapshot(st.saved, st.nd, d)) {
+    o.iters[st.k] = static_cast<uint32_t>(st.iter + 1);
+    o.reason[st.k] = PCR_NOT_CONVERGED;
+    return false;
+  }
+  take_snapshot(st.last[slot], st.nd, d);
+  if (++st.lam == st.power) {
+    st.saved = st.last[slot];
+    st.power <<= 1;
+    st.lam = 0;
+  }
+  ++st.iter;
+  return true;
+}
+
+// reproject's set-up (refine.cpp:80-90): 0 = missed (degenerate direction), 1 = the
+// same-label pass is the label run [j0, j0 + len) of the 3x3x3 neighbourhood list,
+// 2 = no neighbourhood list for this box (serial reproject)
+__device__ __forceinline__ int reproject_setup(const V3& prev, const V3& predicted, uint32_t label, const GridView& g,
+                                               V3& dir, uint32_t& j0, uint32_t& len) {
+  const V3 diff = predicted - prev;
+  const double dist = norm(diff);
+  if (dist < kTiny) return 0;
+  dir = diff / dist;
+  if (g.nb_off == nullptr) return 2;
+  const double radius = 2.0 * g.sub_edge;
+  const double pc[3] = {predicted.x, predicted.y, predicted.z};
+  const double oc[3] = {g.origin.x, g.origin.y, g.origin.z};
+  int cc[3];
+  for (int a = 0; a < 3; ++a) {
+    const int l = voxel_floor(pc[a] - radius, oc[a], g.voxel_size);
+    const int h = voxel_floor(pc[a] + radius, oc[a], g.voxel_size);
+    cc[a] = l + 1;
+    if (!(h == l + 2 && cc[a] >= 0 && cc[a] < g.dims[a])) return 2;
+  }
+  const uint32_t c = linear_index(g, cc[0], cc[1], cc[2]);
+  uint32_t lo = g.nb_off[c], hi = g.nb_off[c + 1];
+  const uint32_t end = hi;
+  while (lo < hi) {
+    const uint32_t m = (lo + hi) >> 1;
+    if (g.nb_lab[m] < label) lo = m + 1; else hi = m;
+  }
+  j0 = lo;
+  hi = end;
+  while (lo < hi) {
+    const uint32_t m = (lo + hi) >> 1;
+    if (g.nb_lab[m] <= label) lo = m + 1; else hi = m;
+  }
+  len = lo - j0;
+  return 1;
+}
+
+// The warp's same-label scans as one flat loop (every lane calls it).
+__device__ __forceinline__ void coop_scan(ScanSlot* ws, uint8_t* owner_at, int lane, uint32_t len, uint32_t j0,
+                                          const V3& prev, const V3& dir, const V3& pred, const GridView& g,
+                                          const SceneView& s, uint32_t& n_march, long long& c_num, long long& c_dn,
+                                          double& c_t) {
+  uint32_t incl = len;
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t v = __shfl_up_sync(kFull, incl, off);
+    if (lane >= off) incl += v;
+  }
+  const uint32_t total = __shfl_sync(kFull, incl, 31);
+  const uint32_t pre = incl - len;
+  ScanSlot& me = ws[lane];
+  me.best_f = kNoRec;
+  if (total == 0) return;
+  if (len) {
+    me.prev[0] = prev.x, me.prev[1] = prev.y, me.prev[2] = prev.z;
+    me.dir[0] = dir.x, me.dir[1] = dir.y, me.dir[2] = dir.z;
+    me.pred[0] = pred.x, me.pred[1] = pred.y, me.pred[2] = pred.z;
+    me.best_t = 1.7976931348623157e308;
+    me.pre = pre;
+    me.j0 = j0;
+  }
+  __syncwarp();
+  const double radius = 2.0 * g.sub_edge;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  int carry = 0;
+  for (uint32_t base = 0; base < total; base += 32) {
+    const bool starts = len && pre >= base && pre - base < 32u;
+    if (starts) owner_at[pre - base] = static_cast<uint8_t>(lane);
+    const uint32_t smask = __reduce_or_sync(kFull, starts ? 1u << (pre - base) : 0u);
+    __syncwarp();
+    const uint32_t F = base + lane;
+    const bool valid = F < total;
+    const uint32_t below = smask & (kFull >> (31 - lane));
+    int o = below ? owner_at[31 - __clz(below)] : carry;
+    double t = inf;
+    if (valid) {
+      const ScanSlot& sl = ws[o];
+      const double4 r4 = g.nb_rec[sl.j0 + (F - sl.pre)];
+      const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r4.w));
+      const uint32_t ie = static_cast<uint32_t>(w >> 33);
+      const V3 sc = ld3(r4);
+      const double rad = g.rr_uniform ? g.rr_radius : g.ie_sc[ie].w;
+      const V3 pq{sl.pred[0], sl.pred[1], sl.pred[2]};
+      if (norm_le(sc - pq, radius + rad)) {
+        ++n_march;  // counts the reference's march_segment call
+        const V3 pv{sl.prev[0], sl.prev[1], sl.prev[2]}, dv{sl.dir[0], sl.dir[1], sl.dir[2]};
+        const double t_center = dot(sc - pv, dv);
+        const double t_lo = smax(0.0, t_center - rad);
+        double bt = sl.best_t;
+        if (t_lo < bt) {
+          if ((w >> 32) & 1u) {
+            if (planar_candidate(pv, dv, ie, g, t_lo, t_center + rad, bt, c_num, c_dn, c_t)) t = bt;
+          } else {
+            SurfaceHit hit;
+            if (march_segment(pv, dv, ie, g, s, inf, &hit) && hit.distance < bt) t = hit.distance;
+          }
+        }
+      }
+    } else {
+      o = 32;  // no record: a segment of its own
+    }
+    // segmented (t, F) min towards each segment's first lane; ties keep the lower F
+    double bt = t;
+    uint32_t bf = F;
+    for (int off = 1; off < 32; off <<= 1) {
+      const double ot = __shfl_down_sync(kFull, bt, off);
+      const uint32_t of = __shfl_down_sync(kFull, bf, off);
+      const int oo = __shfl_down_sync(kFull, o, off);
+      if (lane + off < 32 && oo == o && ot < bt) {
+        bt = ot;
+        bf = of;
+      }
+    }
+    const int op = __shfl_up_sync(kFull, o, 1);
+    carry = __shfl_sync(kFull, o, 31);
+    __syncwarp();
+    if (valid && (lane == 0 || op != o) && bt < ws[o].best_t) {
+      ws[o].best_t = bt;
+      ws[o].best_f = bf;
+    }
+    __syncwarp();
+  }
+}
+
+template <int D, int kMinBlocks>
+__global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
+    refine_warp_kernel(CandIn in, uint32_t n, GridView g, SceneView s, double delta, int rho, double step_size,
+                       RefOut o, uint32_t* next_cand) {
+  __shared__ ScanSlot slots[kRefineThreads];
+  __shared__ uint8_t owner_at[kRefineThreads];
+  const int lane = threadIdx.x & 31;
+  ScanSlot* ws = slots + (threadIdx.x & ~31u);
+  uint8_t* oa = owner_at + (threadIdx.x & ~31u);
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  PathState<D> st;
+  bool active = false, open = true;
+  uint32_t n_trials = 0, n_march = 0;
+  long long c_num = 0x7ff8dead7ff8deadll, c_dn = 0x7ff8dead7ff8deadll;
+  double c_t = 0.0;
+  for (;;) {
+    while (!active && open) {
+      const uint32_t idx = atomicAdd(next_cand, 1u);
+      if (idx >= n) {
+        open = false;
+        break;
+      }
+      active = path_init(st, in.first + idx * in.step, in, s, o);
+    }
+    if (!__any_sync(kFull, active)) break;
+    bool alive = active && path_step_a(st, in, g, s, delta, rho, step_size, o, n_trials);
+    // reprojection, front to back (refine.cpp:234-250), node index by node index
+    for (int q = 0; q < D; ++q) {
+      bool need = alive && q < st.d && st.nd[q].kind == 0;
+      if (!__any_sync(kFull, need)) continue;
+      V3 prev{}, pred{}, dir{};
+      uint32_t j0 = 0, len = 0;
+      bool coop = false;
+      Reproj re;
+      bool got = false;
+      if (need) {
+        prev = q == 0 ? st.tx : node_point(st.nd[q - 1], st.nd[q - 1].p0, st.nd[q - 1].p1);
+        pred = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
+        const int r = reproject_setup(prev, pred, st.nd[q].label, g, dir, j0, len);
+        if (r == 1) {
+          coop = true;
+        } else if (r == 2) {
+          got = reproject(prev, pred, st.nd[q].label, g, s, re, n_march);
+        }
+      }
+      coop_scan(ws, oa, lane, coop ? len : 0u, j0, prev, dir, pred, g, s, n_march, c_num, c_dn, c_t);
+      if (coop) {
+        const uint32_t bf = ws[lane].best_f;
+        if (bf != kNoRec) {
+          const double bt = ws[lane].best_t;
+          const uint32_t ie =
+              static_cast<uint32_t>(static_cast<uint64_t>(__double_as_longlong(g.nb_rec[j0 + (bf - ws[lane].pre)].w)) >> 33);
+          if (ie_planar(g, ie)) {  // make_hit's record (surface.cpp:98-106)
+            re = Reproj{prev + bt * dir, ld3(g.ie_pn[ie]), g.ie_label[ie]};
+          } else {
+            SurfaceHit hit;
+            march_segment(prev, dir, ie, g, s, inf, &hit);
+            re = Reproj{hit.position, hit.normal, g.ie_label[ie]};
+          }
+          polish(re, ie, g, s);
+          got = true;
+        } else {
+          got = reproject(prev, pred, st.nd[q].label, g, s, re, n_march, 1);
+        }
+      }
+      if (need) {
+        if (!got) {
+          o.reason[st.k] = PCR_RAY_MISSED;
+          o.iters[st.k] = static_cast<uint32_t>(st.iter + 1);
+          alive = false;
+        } else {
+          RNode& x = st.nd[q];
+          x.c = re.pos;
+          x.n = re.nrm;
+          local_frame(re.nrm, x.a, x.b);
+          x.p0 = 0.0;
+          x.p1 = 0.0;
+          x.label = re.label;
+        }
+      }
+    }
+    if (alive) alive = path_step_c(st, o);
+    active = alive;
+  }
+  atomicAdd(o.stats, static_cast<unsigned long long>(n_trials));
+  atomicAdd(o.stats + 1, static_cast<unsigned long long>(n_march));
+}
+
+int refine_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("PCR_REFINE_MODE");  // 1 = thread per path (A/B aid)
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+
 // refinement scan records: {sphere centre, label | meta << 32}; flags any IE whose
 // sphere radius differs (bitwise) from the first one's
 __global__ void refine_records_kernel(GridView g, double4* __restrict__ rr, int* __restrict__ nonuniform) {
@@ -725,17 +1153,23 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
   count_launch();
   {
     KTimer kt(ctx, "refine");
+    const char* trace = std::getenv("PCR_REFINE_TRACE");
     // enough resident threads to fill every SM at the kernel's occupancy
     int per_sm = 0;
     // depth bound of this batch: the smallest instantiation that holds its stride
     // (4 blocks of 128 threads per SM, 128 registers: measured faster than 168 or 255
     // registers per thread, which cut the spill traffic but halve the resident warps)
-    auto kern = in.stride <= 3 ? refine_kernel<3, 4> : in.stride <= 5 ? refine_kernel<5, 4> : refine_kernel<kMaxDepth, 4>;
-    PCR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, 0));
+    const bool warp = refine_mode() == 0 && !trace;
+    auto kern = in.stride <= 3 ? refine_warp_kernel<3, 4> : in.stride <= 5 ? refine_warp_kernel<5, 4>
+                                                                           : refine_warp_kernel<kMaxDepth, 4>;
+    auto kern2 = in.stride <= 3 ? refine_kernel<3, 4> : in.stride <= 5 ? refine_kernel<5, 4> : refine_kernel<kMaxDepth, 4>;
+    if (warp)
+      PCR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, 0));
+    else
+      PCR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern2, kRefineThreads, 0));
     const uint64_t want = (static_cast<uint64_t>(n_sub) + kRefineThreads - 1) / kRefineThreads;
     const uint64_t cap = static_cast<uint64_t>(ctx.sm_count) * (per_sm > 0 ? per_sm : 1);
     const unsigned grid_n = static_cast<unsigned>(want < cap ? want : cap);
-    const char* trace = std::getenv("PCR_REFINE_TRACE");
     DBuf<unsigned long long> dbg;
     unsigned long long t0 = 0;
     if (trace) {
@@ -747,8 +1181,11 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
       t0 = static_cast<unsigned long long>(std::chrono::duration_cast<std::chrono::nanoseconds>(
           std::chrono::system_clock::now().time_since_epoch()).count());
     }
-    kern<<<grid_n, kRefineThreads, 0, s>>>(
-        ci, n_sub, gv, scene.view(), p.delta, p.rho, p.step_size, ro, next.get(), rev_order());
+    if (warp)
+      kern<<<grid_n, kRefineThreads, 0, s>>>(ci, n_sub, gv, scene.view(), p.delta, p.rho, p.step_size, ro, next.get());
+    else
+      kern2<<<grid_n, kRefineThreads, 0, s>>>(
+          ci, n_sub, gv, scene.view(), p.delta, p.rho, p.step_size, ro, next.get(), rev_order());
     if (trace) {
       std::vector<unsigned long long> h(3ull * grid_n * kRefineThreads);
       d2h(h.data(), dbg.get(), h.size(), s);
