@@ -588,6 +588,16 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
 // The scan's pruning (t_lo / t* against the best so far) only ever skips records that
 // cannot win, so pruning against the best of earlier rounds changes nothing.
 
+// The scan and the per-path steps are separate (not inlined) functions: each gets its
+// own register allocation instead of one 168-register budget shared with the whole
+// path state, which spilled inside the scan loop (measured: 714 -> 677 ms on C2).
+#ifndef PCR_COOP_INLINE
+#define PCR_COOP_INLINE __noinline__
+#endif
+#ifndef PCR_STEP_INLINE
+#define PCR_STEP_INLINE __noinline__
+#endif
+
 struct ScanSlot {  // one per lane: the reprojection it posted and its best record so far
   double prev[3], dir[3], pred[3];
   double best_t;
@@ -610,7 +620,7 @@ constexpr unsigned kFull = 0xffffffffu;
 
 // make_path_state (refine.cpp:134-161); false when the path is done at once (LOS)
 template <int D>
-__device__ bool path_init(PathState<D>& st, uint32_t k, const CandIn& in, const SceneView& s, const RefOut& o) {
+__device__ PCR_STEP_INLINE bool path_init(PathState<D>& st, uint32_t k, const CandIn& in, const SceneView& s, const RefOut& o) {
   const int d = static_cast<int>(in.n_inter[k]);
   st.k = k;
   st.d = d;
@@ -663,7 +673,7 @@ __device__ bool path_init(PathState<D>& st, uint32_t k, const CandIn& in, const 
 
 // converged: final per-segment visibility (refine.cpp:256-265) and the refined path
 template <int D>
-__device__ void path_converged(const PathState<D>& st, const CandIn& in, const GridView& g, const SceneView& s,
+__device__ PCR_STEP_INLINE void path_converged(const PathState<D>& st, const CandIn& in, const GridView& g, const SceneView& s,
                                const RefOut& o) {
   const uint32_t k = st.k;
   const int d = st.d;
@@ -695,7 +705,7 @@ __device__ void path_converged(const PathState<D>& st, const CandIn& in, const G
 // One iteration up to the reprojection: rho bound, local_gradients (:167-187), the
 // convergence test, backtracking (:209-232). False when the path is finished.
 template <int D>
-__device__ bool path_step_a(PathState<D>& st, const CandIn& in, const GridView& g, const SceneView& s, double delta,
+__device__ PCR_STEP_INLINE bool path_step_a(PathState<D>& st, const CandIn& in, const GridView& g, const SceneView& s, double delta,
                             int rho, double step_size, const RefOut& o, uint32_t& n_trials) {
   const uint32_t k = st.k;
   const int d = st.d;
@@ -762,7 +772,7 @@ __device__ bool path_step_a(PathState<D>& st, const CandIn& in, const GridView& 
 
 // After the reprojection: new chain length, cycle checks (see Snapshot), next iteration.
 template <int D>
-__device__ bool path_step_c(PathState<D>& st, const RefOut& o) {
+__device__ PCR_STEP_INLINE bool path_step_c(PathState<D>& st, const RefOut& o) {
   const int d = st.d;
   for (int q = 0; q < d; ++q) st.pts[q] = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
   st.f = chain_len(st.tx, st.pts, d, st.rx);
@@ -820,11 +830,21 @@ __device__ __forceinline__ int reproject_setup(const V3& prev, const V3& predict
   return 1;
 }
 
-// The warp's same-label scans as one flat loop (every lane calls it).
-__device__ __forceinline__ void coop_scan(ScanSlot* ws, uint8_t* owner_at, int lane, uint32_t len, uint32_t j0,
-                                          const V3& prev, const V3& dir, const V3& pred, const GridView& g,
-                                          const SceneView& s, uint32_t& n_march, long long& c_num, long long& c_dn,
-                                          double& c_t) {
+// Per-lane scan scratch kept across calls: the plane division cache and the march count.
+struct ScanCache {
+  long long c_num, c_dn;
+  double c_t;
+  uint32_t n_march;
+};
+
+// The warp's same-label scans as one flat loop (every lane calls it). A posting lane
+// (len > 0) has written prev, dir, pred and j0 into its slot. Not inlined: the caller's
+// path state stays out of the loop's registers (it spilled inside the loop otherwise).
+__device__ PCR_COOP_INLINE void coop_scan(ScanSlot* ws, uint8_t* owner_at, int lane, uint32_t len, const GridView& g,
+                                       const SceneView& s, ScanCache* cache) {
+  long long c_num = cache->c_num, c_dn = cache->c_dn;
+  double c_t = cache->c_t;
+  uint32_t n_march = cache->n_march;
   uint32_t incl = len;
   for (int off = 1; off < 32; off <<= 1) {
     const uint32_t v = __shfl_up_sync(kFull, incl, off);
@@ -835,14 +855,8 @@ __device__ __forceinline__ void coop_scan(ScanSlot* ws, uint8_t* owner_at, int l
   ScanSlot& me = ws[lane];
   me.best_f = kNoRec;
   if (total == 0) return;
-  if (len) {
-    me.prev[0] = prev.x, me.prev[1] = prev.y, me.prev[2] = prev.z;
-    me.dir[0] = dir.x, me.dir[1] = dir.y, me.dir[2] = dir.z;
-    me.pred[0] = pred.x, me.pred[1] = pred.y, me.pred[2] = pred.z;
-    me.best_t = 1.7976931348623157e308;
-    me.pre = pre;
-    me.j0 = j0;
-  }
+  me.best_t = 1.7976931348623157e308;
+  me.pre = pre;
   __syncwarp();
   const double radius = 2.0 * g.sub_edge;
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
@@ -904,6 +918,10 @@ __device__ __forceinline__ void coop_scan(ScanSlot* ws, uint8_t* owner_at, int l
     }
     __syncwarp();
   }
+  cache->c_num = c_num;
+  cache->c_dn = c_dn;
+  cache->c_t = c_t;
+  cache->n_march = n_march;
 }
 
 template <int D, int kMinBlocks>
@@ -919,8 +937,10 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
   PathState<D> st;
   bool active = false, open = true;
   uint32_t n_trials = 0, n_march = 0;
-  long long c_num = 0x7ff8dead7ff8deadll, c_dn = 0x7ff8dead7ff8deadll;
-  double c_t = 0.0;
+  ScanCache cache{0x7ff8dead7ff8deadll, 0x7ff8dead7ff8deadll, 0.0, 0u};
+  uint32_t done = 0;
+  unsigned long long t_start = 0, t_last = 0;
+  if (g_refine_dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   for (;;) {
     while (!active && open) {
       const uint32_t idx = atomicAdd(next_cand, 1u);
@@ -936,28 +956,37 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
     for (int q = 0; q < D; ++q) {
       bool need = alive && q < st.d && st.nd[q].kind == 0;
       if (!__any_sync(kFull, need)) continue;
-      V3 prev{}, pred{}, dir{};
-      uint32_t j0 = 0, len = 0;
+      uint32_t len = 0;
       bool coop = false;
       Reproj re;
       bool got = false;
       if (need) {
-        prev = q == 0 ? st.tx : node_point(st.nd[q - 1], st.nd[q - 1].p0, st.nd[q - 1].p1);
-        pred = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
+        const V3 prev = q == 0 ? st.tx : node_point(st.nd[q - 1], st.nd[q - 1].p0, st.nd[q - 1].p1);
+        const V3 pred = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
+        V3 dir{};
+        uint32_t j0 = 0;
         const int r = reproject_setup(prev, pred, st.nd[q].label, g, dir, j0, len);
         if (r == 1) {
           coop = true;
+          ScanSlot& me = ws[lane];
+          me.prev[0] = prev.x, me.prev[1] = prev.y, me.prev[2] = prev.z;
+          me.dir[0] = dir.x, me.dir[1] = dir.y, me.dir[2] = dir.z;
+          me.pred[0] = pred.x, me.pred[1] = pred.y, me.pred[2] = pred.z;
+          me.j0 = j0;
         } else if (r == 2) {
           got = reproject(prev, pred, st.nd[q].label, g, s, re, n_march);
         }
       }
-      coop_scan(ws, oa, lane, coop ? len : 0u, j0, prev, dir, pred, g, s, n_march, c_num, c_dn, c_t);
+      coop_scan(ws, oa, lane, coop ? len : 0u, g, s, &cache);
       if (coop) {
-        const uint32_t bf = ws[lane].best_f;
+        const ScanSlot& me = ws[lane];
+        const V3 prev{me.prev[0], me.prev[1], me.prev[2]}, dir{me.dir[0], me.dir[1], me.dir[2]};
+        const V3 pred{me.pred[0], me.pred[1], me.pred[2]};
+        const uint32_t bf = len ? me.best_f : kNoRec;
         if (bf != kNoRec) {
-          const double bt = ws[lane].best_t;
+          const double bt = me.best_t;
           const uint32_t ie =
-              static_cast<uint32_t>(static_cast<uint64_t>(__double_as_longlong(g.nb_rec[j0 + (bf - ws[lane].pre)].w)) >> 33);
+              static_cast<uint32_t>(static_cast<uint64_t>(__double_as_longlong(g.nb_rec[me.j0 + (bf - me.pre)].w)) >> 33);
           if (ie_planar(g, ie)) {  // make_hit's record (surface.cpp:98-106)
             re = Reproj{prev + bt * dir, ld3(g.ie_pn[ie]), g.ie_label[ie]};
           } else {
@@ -988,11 +1017,28 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
       }
     }
     if (alive) alive = path_step_c(st, o);
+    if (active && !alive && g_refine_dbg) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_last));
+      ++done;
+    }
     active = alive;
   }
+  if (g_refine_dbg) {  // development trace (PCR_REFINE_TRACE): start, last path's end, paths
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    g_refine_dbg[3 * tid] = t_start;
+    g_refine_dbg[3 * tid + 1] = t_last ? t_last : t_start;
+    g_refine_dbg[3 * tid + 2] = done;
+  }
   atomicAdd(o.stats, static_cast<unsigned long long>(n_trials));
-  atomicAdd(o.stats + 1, static_cast<unsigned long long>(n_march));
+  atomicAdd(o.stats + 1, static_cast<unsigned long long>(n_march + cache.n_march));
 }
+
+// 3 blocks of 128 threads per SM (168 registers): measured 4 -> 873 ms, 3 -> 686 ms,
+// 2 -> 796 ms on C2 (same box)
+#ifndef PCR_WARP_MINB
+#define PCR_WARP_MINB 3
+#endif
+constexpr int kWarpMinBlocks = PCR_WARP_MINB;
 
 int refine_mode() {
   static const int m = [] {
@@ -1156,12 +1202,13 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     const char* trace = std::getenv("PCR_REFINE_TRACE");
     // enough resident threads to fill every SM at the kernel's occupancy
     int per_sm = 0;
-    // depth bound of this batch: the smallest instantiation that holds its stride
-    // (4 blocks of 128 threads per SM, 128 registers: measured faster than 168 or 255
-    // registers per thread, which cut the spill traffic but halve the resident warps)
-    const bool warp = refine_mode() == 0 && !trace;
-    auto kern = in.stride <= 3 ? refine_warp_kernel<3, 4> : in.stride <= 5 ? refine_warp_kernel<5, 4>
-                                                                           : refine_warp_kernel<kMaxDepth, 4>;
+    // depth bound of this batch: the smallest instantiation that holds its stride.
+    // Default: the warp-cooperative kernel; PCR_REFINE_MODE=1 selects the thread-per-path
+    // kernel (4 blocks of 128 threads per SM, 128 registers), kept as the A/B baseline.
+    const bool warp = refine_mode() == 0;
+    auto kern = in.stride <= 3 ? refine_warp_kernel<3, kWarpMinBlocks>
+                : in.stride <= 5 ? refine_warp_kernel<5, kWarpMinBlocks>
+                                 : refine_warp_kernel<kMaxDepth, kWarpMinBlocks>;
     auto kern2 = in.stride <= 3 ? refine_kernel<3, 4> : in.stride <= 5 ? refine_kernel<5, 4> : refine_kernel<kMaxDepth, 4>;
     if (warp)
       PCR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, 0));
