@@ -49,6 +49,8 @@ struct GridView {
   const uint32_t* nb_off = nullptr;  // n_cells + 1
   const double4* nb_rec = nullptr;
   const uint32_t* nb_lab = nullptr;  // label of each list entry (lists are stably sorted by label)
+  const double4* nb_pa = nullptr;    // per entry: plane point, sphere radius
+  const double4* nb_pb = nullptr;    // per entry: plane normal
 };
 
 // Device-resident Scene (scene.hpp:38-46).

@@ -79,11 +79,10 @@ __device__ __forceinline__ int voxel_floor(double p, double o, double vs) {
 // (same normal and plane-offset bits, e.g. the IEs of one wall) share t*: the
 // division is done once per plane (cache c_num, c_dn -> c_t). Returns true and
 // lowers best_t when this IE's hit is strictly nearer.
-__device__ __forceinline__ bool planar_candidate(const V3& prev, const V3& dir, uint32_t ie, const GridView& g,
-                                                 double t_lo, double t_hi, double& best_t, long long& c_num,
-                                                 long long& c_dn, double& c_t) {
+__device__ __forceinline__ bool planar_candidate_at(const V3& prev, const V3& dir, const V3& pp, const V3& pn,
+                                                    double eps, double t_lo, double t_hi, double& best_t,
+                                                    long long& c_num, long long& c_dn, double& c_t) {
   if (t_hi <= t_lo) return false;
-  const V3 pp = ld3(g.ie_pp[ie]), pn = ld3(g.ie_pn[ie]);
   const double dn = dot(dir, pn);
   const bool snap = fabs(dn) > 1e-12;
   double t_star = 0.0;
@@ -99,7 +98,6 @@ __device__ __forceinline__ bool planar_candidate(const V3& prev, const V3& dir, 
   }
   const bool in_win = snap && t_star >= t_lo && t_star <= t_hi;
   if (in_win && t_star >= best_t) return false;
-  const double eps = g.hit_eps;
   double tc;
   const double f = dot((prev + t_lo * dir) - pp, pn);
   if (fabs(f) <= eps) {
@@ -117,6 +115,13 @@ __device__ __forceinline__ bool planar_candidate(const V3& prev, const V3& dir, 
   if (t >= best_t) return false;
   best_t = t;
   return true;
+}
+__device__ __forceinline__ bool planar_candidate(const V3& prev, const V3& dir, uint32_t ie, const GridView& g,
+                                                 double t_lo, double t_hi, double& best_t, long long& c_num,
+                                                 long long& c_dn, double& c_t) {
+  if (t_hi <= t_lo) return false;
+  return planar_candidate_at(prev, dir, ld3(g.ie_pp[ie]), ld3(g.ie_pn[ie]), g.hit_eps, t_lo, t_hi, best_t, c_num,
+                             c_dn, c_t);
 }
 
 // reproject (refine.cpp:80-130) with surface_ies_near (:34-52) scanned in place.
@@ -873,11 +878,15 @@ __device__ PCR_COOP_INLINE void coop_scan(ScanSlot* ws, uint8_t* owner_at, int l
     double t = inf;
     if (valid) {
       const ScanSlot& sl = ws[o];
-      const double4 r4 = g.nb_rec[sl.j0 + (F - sl.pre)];
+      const uint32_t j = sl.j0 + (F - sl.pre);
+      // the record and its plane side by side (no dependent load through the IE index)
+      const double4 r4 = g.nb_rec[j];
+      const double4 pa = g.nb_pa[j];
+      const double4 pb = g.nb_pb[j];
       const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r4.w));
       const uint32_t ie = static_cast<uint32_t>(w >> 33);
       const V3 sc = ld3(r4);
-      const double rad = g.rr_uniform ? g.rr_radius : g.ie_sc[ie].w;
+      const double rad = pa.w;
       const V3 pq{sl.pred[0], sl.pred[1], sl.pred[2]};
       if (norm_le(sc - pq, radius + rad)) {
         ++n_march;  // counts the reference's march_segment call
@@ -887,7 +896,9 @@ __device__ PCR_COOP_INLINE void coop_scan(ScanSlot* ws, uint8_t* owner_at, int l
         double bt = sl.best_t;
         if (t_lo < bt) {
           if ((w >> 32) & 1u) {
-            if (planar_candidate(pv, dv, ie, g, t_lo, t_center + rad, bt, c_num, c_dn, c_t)) t = bt;
+            if (planar_candidate_at(pv, dv, ld3(pa), ld3(pb), g.hit_eps, t_lo, t_center + rad, bt, c_num, c_dn,
+                                    c_t))
+              t = bt;
           } else {
             SurfaceHit hit;
             if (march_segment(pv, dv, ie, g, s, inf, &hit) && hit.distance < bt) t = hit.distance;
@@ -1112,6 +1123,18 @@ __global__ void nb_fill_kernel(GridView g, const uint32_t* __restrict__ off, dou
   }
 }
 
+// plane of each neighbourhood-list entry, in list order: {plane point, sphere radius},
+// {plane normal, 0} (the warp kernel's scan reads them beside the record)
+__global__ void nb_geo_kernel(GridView g, uint32_t total, const double4* __restrict__ rec, double4* __restrict__ pa,
+                              double4* __restrict__ pb) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= total) return;
+  const uint32_t ie = static_cast<uint32_t>(static_cast<uint64_t>(__double_as_longlong(rec[j].w)) >> 33);
+  const double4 pp = g.ie_pp[ie], pn = g.ie_pn[ie];
+  pa[j] = make_double4(pp.x, pp.y, pp.z, g.rr_uniform ? g.rr_radius : g.ie_sc[ie].w);
+  pb[j] = make_double4(pn.x, pn.y, pn.z, 0.0);
+}
+
 int rev_order() {
   static const int r = [] {
     const char* e = std::getenv("PCR_REFINE_REV");
@@ -1168,7 +1191,7 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
   // neighbourhood lists (the reprojection box is a cell's 3x3x3 neighbourhood whenever
   // 2 * subvoxel_edge spans exactly one voxel each way, i.e. division_factor 2)
   DBuf<uint32_t> nb_off, nb_lab;
-  DBuf<double4> nb_rec;
+  DBuf<double4> nb_rec, nb_pa, nb_pb;
   if (grid.n_cells && grid.n_ies && grid.n_ies < (1ull << 31) && grid.n_cells < (1ull << 31)) {
     const uint32_t nc = static_cast<uint32_t>(grid.n_cells);
     DBuf<uint32_t> cnt(nc, s), tot(1, s);
@@ -1185,9 +1208,18 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     count_launch();
     nb_fill_kernel<<<nb(nc, 256), 256, 0, s>>>(gv, nb_off.get(), nb_rec.get(), nb_lab.get());
     PCR_LAUNCH_CHECK();
+    nb_pa.alloc(total ? total : 1, s);
+    nb_pb.alloc(total ? total : 1, s);
+    if (total) {
+      count_launch();
+      nb_geo_kernel<<<nb(total, 256), 256, 0, s>>>(gv, total, nb_rec.get(), nb_pa.get(), nb_pb.get());
+      PCR_LAUNCH_CHECK();
+    }
     gv.nb_off = nb_off.get();
     gv.nb_rec = nb_rec.get();
     gv.nb_lab = nb_lab.get();
+    gv.nb_pa = nb_pa.get();
+    gv.nb_pb = nb_pb.get();
   }
   CandIn ci{in.first, step, in.stride, in.tx, in.rx, in.n_inter, in.kind, in.pos, in.label, in.nrm, in.edge, in.coarse_length};
   DBuf<unsigned long long> stats(2, s);
