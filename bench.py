@@ -132,7 +132,7 @@ def roofline(kernel, ms_total, launches, summary, mean_depth, peaks, peaks_kind,
         achieved = per_launch / (ms_total / max(launches, 1) * 1e-3) / 1e12
         return {"bound": "fp64", "kernel": kernel, "achieved": achieved, "peak": fp64_tflops, "unit": "TFLOP/s",
                 "frac": achieved / fp64_tflops if fp64_tflops else None, "traffic": measured_traffic(kernel),
-                "traffic_note": "DRAM bytes per launch (ncu, profiles/ncu_traffic.json): spilled local memory; "
+                "traffic_note": "DRAM bytes per launch (ncu, profiles/ncu_traffic.json): per-lane local memory (path state, call frames); "
                                 "the kernel's algorithmic inputs are L2-resident",
                 "algorithmic_per_launch": per_launch, "avg_launch_ms": ms_total / max(launches, 1),
                 "peak_source": "in-run non-FMA FP64 probe (pcr_fp64_probe); MEASURED_PEAKS.json has no FP64 figure"}
