@@ -842,11 +842,36 @@ struct ScanCache {
   uint32_t n_march;
 };
 
+// the warps' scan slots and round owner maps (file scope, so the out-of-line scan
+// addresses them as shared memory rather than through generic pointers)
+__shared__ ScanSlot g_slots[kRefineThreads];
+__shared__ uint8_t g_owner_at[kRefineThreads];
+
+// A non-planar record of the cooperative scan: its march_segment distance when it is a
+// hit nearer than bt, else +inf. Out of line with the vectors passed by value: taking
+// their address for march_segment put the scan's vectors in local memory every round.
+__device__ __noinline__ double march_np(double px, double py, double pz, double dx, double dy, double dz, uint32_t ie,
+                                        const GridView& g, const SceneView& s, double bt) {
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  const V3 pv{px, py, pz}, dv{dx, dy, dz};
+  SurfaceHit hit;
+  if (march_segment(pv, dv, ie, g, s, inf, &hit) && hit.distance < bt) return hit.distance;
+  return inf;
+}
+
 // The warp's same-label scans as one flat loop (every lane calls it). A posting lane
 // (len > 0) has written prev, dir, pred and j0 into its slot. Not inlined: the caller's
 // path state stays out of the loop's registers (it spilled inside the loop otherwise).
-__device__ PCR_COOP_INLINE void coop_scan(ScanSlot* ws, uint8_t* owner_at, int lane, uint32_t len, const GridView& g,
-                                       const SceneView& s, ScanCache* cache) {
+__device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView& g, const SceneView& s,
+                                          ScanCache* cache) {
+  const uint32_t wb = threadIdx.x & ~31u;
+  ScanSlot* ws = g_slots + wb;
+  uint8_t* owner_at = g_owner_at + wb;
+  // the grid fields the loop reads, in registers (g is a reference into the caller's frame)
+  const double4* __restrict__ nb_rec = g.nb_rec;
+  const double4* __restrict__ nb_pa = g.nb_pa;
+  const double4* __restrict__ nb_pb = g.nb_pb;
+  const double eps = g.hit_eps;
   long long c_num = cache->c_num, c_dn = cache->c_dn;
   double c_t = cache->c_t;
   uint32_t n_march = cache->n_march;
@@ -880,9 +905,9 @@ __device__ PCR_COOP_INLINE void coop_scan(ScanSlot* ws, uint8_t* owner_at, int l
       const ScanSlot& sl = ws[o];
       const uint32_t j = sl.j0 + (F - sl.pre);
       // the record and its plane side by side (no dependent load through the IE index)
-      const double4 r4 = g.nb_rec[j];
-      const double4 pa = g.nb_pa[j];
-      const double4 pb = g.nb_pb[j];
+      const double4 r4 = nb_rec[j];
+      const double4 pa = nb_pa[j];
+      const double4 pb = nb_pb[j];
       const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r4.w));
       const uint32_t ie = static_cast<uint32_t>(w >> 33);
       const V3 sc = ld3(r4);
@@ -896,12 +921,10 @@ __device__ PCR_COOP_INLINE void coop_scan(ScanSlot* ws, uint8_t* owner_at, int l
         double bt = sl.best_t;
         if (t_lo < bt) {
           if ((w >> 32) & 1u) {
-            if (planar_candidate_at(pv, dv, ld3(pa), ld3(pb), g.hit_eps, t_lo, t_center + rad, bt, c_num, c_dn,
-                                    c_t))
+            if (planar_candidate_at(pv, dv, ld3(pa), ld3(pb), eps, t_lo, t_center + rad, bt, c_num, c_dn, c_t))
               t = bt;
           } else {
-            SurfaceHit hit;
-            if (march_segment(pv, dv, ie, g, s, inf, &hit) && hit.distance < bt) t = hit.distance;
+            t = march_np(pv.x, pv.y, pv.z, dv.x, dv.y, dv.z, ie, g, s, bt);
           }
         }
       }
@@ -939,11 +962,8 @@ template <int D, int kMinBlocks>
 __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
     refine_warp_kernel(CandIn in, uint32_t n, GridView g, SceneView s, double delta, int rho, double step_size,
                        RefOut o, uint32_t* next_cand) {
-  __shared__ ScanSlot slots[kRefineThreads];
-  __shared__ uint8_t owner_at[kRefineThreads];
   const int lane = threadIdx.x & 31;
-  ScanSlot* ws = slots + (threadIdx.x & ~31u);
-  uint8_t* oa = owner_at + (threadIdx.x & ~31u);
+  ScanSlot* ws = g_slots + (threadIdx.x & ~31u);
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   PathState<D> st;
   bool active = false, open = true;
@@ -988,7 +1008,7 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
           got = reproject(prev, pred, st.nd[q].label, g, s, re, n_march);
         }
       }
-      coop_scan(ws, oa, lane, coop ? len : 0u, g, s, &cache);
+      coop_scan(lane, coop ? len : 0u, g, s, &cache);
       if (coop) {
         const ScanSlot& me = ws[lane];
         const V3 prev{me.prev[0], me.prev[1], me.prev[2]}, dir{me.dir[0], me.dir[1], me.dir[2]};
