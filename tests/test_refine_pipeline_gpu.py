@@ -189,3 +189,44 @@ def test_config_hash_matches(oracle, gpu):
     for kw in [{}, {"kappa": 99}, {"fresnel_enabled": False}, {"voxel_size_m": 0.25}, {"thread_count": 8}]:
         c = abi.default_run_config(**kw)
         assert pcray.config_hash(c) == oracle.config_hash(c)
+
+
+@pytest.mark.parametrize("vs,dv", [(0.5, 1), (0.5, 4), (0.25, 2), (0.3, 3)])
+def test_refine_voxel_params(oracle, gpu, vs, dv):
+    """The warp kernel's cooperative same-label scan applies when the reprojection box is
+    a cell's 3x3x3 neighbourhood (division_factor 2); other grids take the serial cell
+    walk per lane. Both against the reference on the same candidates."""
+    sc = make_scene(box_room((2, 2, 2), 0.05), tx=[(0.6, 0.7, 0.9)], rx=[(1.3, 1.2, 1.1)])
+    vp = abi.voxel_params(vs, dv)
+    rs = oracle.RefScene(sc)
+    rg = oracle.build_grid(rs, vp)
+    ds = pcray.DeviceScene(sc)
+    dg = pcray.build_grid(ds, vp)
+    tp = abi.trace_params(max_interactions=3, max_diffractions=0)
+    _, hits = oracle.transmission_phase(rg, rs, 0, tp)
+    cands = oracle.propagate(rg, rs, 0, hits, tp)
+    assert cands["n"] > 0
+    compare_outcomes(pcray.refine_paths(cands, dg, ds), oracle.refine_batch(rg, rs, cands))
+
+
+def test_refine_kernels_agree():
+    """The warp-cooperative kernel (default) and the thread-per-path kernel
+    (PCR_REFINE_MODE=1) give the same RunSummary, counters included (C2 at depth 2)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = ("import json,sys; sys.path.insert(0, %r); from paper_2402_13747_b200 import abi, pcray, scenes; "
+            "s, _ = scenes.build_scene('C2'); r = pcray.run_pipeline_on_scene(s, abi.default_run_config("
+            "max_interactions=2, max_diffractions=1)); p = r['paths']; "
+            "print(json.dumps([r['coarse_paths'], r['refined_paths'], list(r['rejected']), r['exact_paths'], "
+            "r['refine_iterations'], r['refine_trials'], r['refine_marches'], p['length'].tolist()]))"
+            % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    out = []
+    for mode in ["0", "1"]:
+        env = dict(os.environ, PCR_REFINE_MODE=mode)
+        res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        out.append(json.loads(res.stdout.strip().splitlines()[-1]))
+    assert out[0] == out[1]
