@@ -322,7 +322,9 @@ struct Snapshot {
 
 template <int D>
 __device__ __forceinline__ void take_snapshot(Snapshot<D>& sn, const RNode* nd, int d) {
-  for (int q = 0; q < d; ++q) {
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    if (q >= d) break;
     if (nd[q].kind == 0) {
       sn.v[q][0] = nd[q].c.x;
       sn.v[q][1] = nd[q].c.y;
@@ -339,7 +341,9 @@ __device__ __forceinline__ void take_snapshot(Snapshot<D>& sn, const RNode* nd, 
 
 template <int D>
 __device__ __forceinline__ bool same_snapshot(const Snapshot<D>& sn, const RNode* nd, int d) {
-  for (int q = 0; q < d; ++q) {
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    if (q >= d) break;
     if (nd[q].kind == 0) {
       if (__double_as_longlong(sn.v[q][0]) != __double_as_longlong(nd[q].c.x) ||
           __double_as_longlong(sn.v[q][1]) != __double_as_longlong(nd[q].c.y) ||
@@ -719,25 +723,44 @@ __device__ PCR_STEP_INLINE bool path_step_a(PathState<D>& st, const CandIn& in, 
     o.reason[k] = PCR_NOT_CONVERGED;
     return false;
   }
-  double gr[2 * D];
-  int ng = 0;
-  for (int q = 0; q < d; ++q) {
-    const V3 prev = q == 0 ? st.tx : st.pts[q - 1];
-    const V3 next = q + 1 == d ? st.rx : st.pts[q + 1];
-    const V3 dp = st.pts[q] - prev;
-    const V3 dn = st.pts[q] - next;
-    const double lp = norm(dp), ln = norm(dn);
-    if (lp < kTiny || ln < kTiny) {
-      o.reason[k] = PCR_DEGENERATE;
-      o.iters[k] = static_cast<uint32_t>(st.iter + 1);
-      return false;
+  // loops unrolled to the depth bound with q < d guards: the per-node values stay in
+  // registers (a runtime-indexed array would live in local memory)
+  double ga[D], gb[D];
+  bool refl[D];
+  V3 pts[D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    if (q < d) {
+      pts[q] = st.pts[q];
+      refl[q] = st.nd[q].kind == 0;
     }
-    const V3 e_sum = dp / lp + dn / ln;
-    gr[ng++] = dot(st.nd[q].a, e_sum);
-    if (st.nd[q].kind == 0) gr[ng++] = dot(st.nd[q].b, e_sum);
   }
-  double gn = 0.0;
-  for (int q = 0; q < ng; ++q) gn += gr[q] * gr[q];
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    if (q < d) {
+      const V3 prev = q == 0 ? st.tx : pts[q > 0 ? q - 1 : 0];
+      const V3 next = (q + 1 < D && q + 1 < d) ? pts[q + 1 < D ? q + 1 : q] : st.rx;
+      const V3 dp = pts[q] - prev;
+      const V3 dn = pts[q] - next;
+      const double lp = norm(dp), ln = norm(dn);
+      if (lp < kTiny || ln < kTiny) {
+        o.reason[k] = PCR_DEGENERATE;
+        o.iters[k] = static_cast<uint32_t>(st.iter + 1);
+        return false;
+      }
+      const V3 e_sum = dp / lp + dn / ln;
+      ga[q] = dot(st.nd[q].a, e_sum);
+      gb[q] = refl[q] ? dot(st.nd[q].b, e_sum) : 0.0;
+    }
+  }
+  double gn = 0.0;  // same order as the reference's gradient vector: (u, v) per reflection, w per edge
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    if (q < d) {
+      gn += ga[q] * ga[q];
+      if (refl[q]) gn += gb[q] * gb[q];
+    }
+  }
   st.gnorm = sqrt(gn);
   if (st.gnorm < delta) {
     o.iters[k] = static_cast<uint32_t>(st.iter + 1);
@@ -745,25 +768,34 @@ __device__ PCR_STEP_INLINE bool path_step_a(PathState<D>& st, const CandIn& in, 
     return false;
   }
   double step = step_size;
-  double tp0[D], tp1[D];
   for (int h = 0; h <= 8; ++h) {
-    int gi = 0;
-    V3 tpts[D];
-    for (int q = 0; q < d; ++q) {
-      if (st.nd[q].kind == 0) {
-        tp0[q] = st.nd[q].p0 - step * gr[gi++];
-        tp1[q] = st.nd[q].p1 - step * gr[gi++];
-      } else {
-        tp0[q] = sclamp(st.nd[q].p0 - step * gr[gi++], st.nd[q].lo, st.nd[q].hi);
-        tp1[q] = st.nd[q].p1;
+    double tp0[D], tp1[D];
+    V3 prev = st.tx;
+    double len = 0.0;  // chain_len over the trial points, same summation order
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      if (q < d) {
+        const RNode& nd = st.nd[q];
+        if (refl[q]) {
+          tp0[q] = nd.p0 - step * ga[q];
+          tp1[q] = nd.p1 - step * gb[q];
+        } else {
+          tp0[q] = sclamp(nd.p0 - step * ga[q], nd.lo, nd.hi);
+          tp1[q] = nd.p1;
+        }
+        const V3 tp = node_point(nd, tp0[q], tp1[q]);
+        len += norm(tp - prev);
+        prev = tp;
       }
-      tpts[q] = node_point(st.nd[q], tp0[q], tp1[q]);
     }
     ++n_trials;
-    if (chain_len(st.tx, tpts, d, st.rx) <= st.f + 1e-15) {
-      for (int q = 0; q < d; ++q) {
-        st.nd[q].p0 = tp0[q];
-        st.nd[q].p1 = tp1[q];
+    if (len + norm(st.rx - prev) <= st.f + 1e-15) {
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        if (q < d) {
+          st.nd[q].p0 = tp0[q];
+          st.nd[q].p1 = tp1[q];
+        }
       }
       return true;
     }
@@ -779,8 +811,18 @@ __device__ PCR_STEP_INLINE bool path_step_a(PathState<D>& st, const CandIn& in, 
 template <int D>
 __device__ PCR_STEP_INLINE bool path_step_c(PathState<D>& st, const RefOut& o) {
   const int d = st.d;
-  for (int q = 0; q < d; ++q) st.pts[q] = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
-  st.f = chain_len(st.tx, st.pts, d, st.rx);
+  V3 prev = st.tx;
+  double len = 0.0;  // chain_len, same summation order
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    if (q < d) {
+      const V3 p = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
+      st.pts[q] = p;
+      len += norm(p - prev);
+      prev = p;
+    }
+  }
+  st.f = len + norm(st.rx - prev);
   const int slot = st.iter & 1;
   if (same_snapshot(st.last[slot ^ 1], st.nd, d) || same_snapshot(st.last[slot], st.nd, d) ||
       same_snapshot(st.saved, st.nd, d)) {
