@@ -613,6 +613,12 @@ struct ScanSlot {  // one per lane: the reprojection it posted and its best reco
   uint32_t pre, j0, best_f, pad;
 };
 
+// A node's last label run: (neighbourhood list, label) -> [j0, j0 + len). Successive
+// iterations mostly reproject into the same cell, so the two binary searches are skipped.
+struct RunCache {
+  uint32_t cell, label, j0, len;
+};
+
 template <int D>
 struct PathState {
   uint32_t k;
@@ -622,6 +628,7 @@ struct PathState {
   RNode nd[D];
   V3 pts[D];
   Snapshot<D> saved, last[2];
+  RunCache rc[D];
 };
 
 constexpr uint32_t kNoRec = 0xffffffffu;
@@ -668,7 +675,10 @@ __device__ PCR_STEP_INLINE bool path_init(PathState<D>& st, uint32_t k, const Ca
       x.n = V3{0, 0, 1};
     }
   }
-  for (int q = 0; q < d; ++q) st.pts[q] = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
+  for (int q = 0; q < d; ++q) {
+    st.pts[q] = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
+    st.rc[q].cell = 0xffffffffu;
+  }
   st.f = chain_len(st.tx, st.pts, d, st.rx);
   st.gnorm = 0.0;
   st.iter = 0;
@@ -844,7 +854,7 @@ __device__ PCR_STEP_INLINE bool path_step_c(PathState<D>& st, const RefOut& o) {
 // same-label pass is the label run [j0, j0 + len) of the 3x3x3 neighbourhood list,
 // 2 = no neighbourhood list for this box (serial reproject)
 __device__ __forceinline__ int reproject_setup(const V3& prev, const V3& predicted, uint32_t label, const GridView& g,
-                                               V3& dir, uint32_t& j0, uint32_t& len) {
+                                               V3& dir, uint32_t& j0, uint32_t& len, RunCache& rc) {
   const V3 diff = predicted - prev;
   const double dist = norm(diff);
   if (dist < kTiny) return 0;
@@ -861,6 +871,11 @@ __device__ __forceinline__ int reproject_setup(const V3& prev, const V3& predict
     if (!(h == l + 2 && cc[a] >= 0 && cc[a] < g.dims[a])) return 2;
   }
   const uint32_t c = linear_index(g, cc[0], cc[1], cc[2]);
+  if (c == rc.cell && label == rc.label) {  // same list and label as this node's last scan
+    j0 = rc.j0;
+    len = rc.len;
+    return 1;
+  }
   uint32_t lo = g.nb_off[c], hi = g.nb_off[c + 1];
   const uint32_t end = hi;
   while (lo < hi) {
@@ -874,6 +889,7 @@ __device__ __forceinline__ int reproject_setup(const V3& prev, const V3& predict
     if (g.nb_lab[m] <= label) lo = m + 1; else hi = m;
   }
   len = lo - j0;
+  rc = RunCache{c, label, j0, len};
   return 1;
 }
 
@@ -1038,7 +1054,7 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
         const V3 pred = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
         V3 dir{};
         uint32_t j0 = 0;
-        const int r = reproject_setup(prev, pred, st.nd[q].label, g, dir, j0, len);
+        const int r = reproject_setup(prev, pred, st.nd[q].label, g, dir, j0, len, st.rc[q]);
         if (r == 1) {
           coop = true;
           ScanSlot& me = ws[lane];
