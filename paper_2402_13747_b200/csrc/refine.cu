@@ -989,22 +989,25 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
     } else {
       o = 32;  // no record: a segment of its own
     }
-    // segmented (t, F) min towards each segment's first lane; ties keep the lower F
+    // segmented (t, F) min towards each segment's first lane; ties keep the lower F.
+    // Segments are the owners' runs within the round: they start at lane 0 and at the
+    // run starts (smask); lanes past the last record (t = +inf) never win.
+    const uint32_t heads = smask | 1u;
+    const uint32_t above = heads & ~(kFull >> (31 - lane));
+    const int seg_end = above ? __ffs(above) - 1 : 32;
     double bt = t;
     uint32_t bf = F;
     for (int off = 1; off < 32; off <<= 1) {
       const double ot = __shfl_down_sync(kFull, bt, off);
       const uint32_t of = __shfl_down_sync(kFull, bf, off);
-      const int oo = __shfl_down_sync(kFull, o, off);
-      if (lane + off < 32 && oo == o && ot < bt) {
+      if (lane + off < seg_end && ot < bt) {
         bt = ot;
         bf = of;
       }
     }
-    const int op = __shfl_up_sync(kFull, o, 1);
     carry = __shfl_sync(kFull, o, 31);
     __syncwarp();
-    if (valid && (lane == 0 || op != o) && bt < ws[o].best_t) {
+    if (valid && ((heads >> lane) & 1u) && bt < ws[o].best_t) {
       ws[o].best_t = bt;
       ws[o].best_f = bf;
     }
