@@ -978,7 +978,7 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
         const double t_lo = smax(0.0, t_center - rad);
         double bt = sl.best_t;
         if (t_lo < bt) {
-          if ((w >> 32) & 1u) {
+          if (__builtin_expect(((w >> 32) & 1u) != 0, 1)) {  // planar records are the common case
             if (planar_candidate_at(pv, dv, ld3(pa), ld3(pb), eps, t_lo, t_center + rad, bt, c_num, c_dn, c_t))
               t = bt;
           } else {
