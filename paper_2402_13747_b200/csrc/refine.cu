@@ -1323,6 +1323,10 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
                 : in.stride <= 5 ? refine_warp_kernel<5, kWarpMinBlocks>
                                  : refine_warp_kernel<kMaxDepth, kWarpMinBlocks>;
     auto kern2 = in.stride <= 3 ? refine_kernel<3, 4> : in.stride <= 5 ? refine_kernel<5, 4> : refine_kernel<kMaxDepth, 4>;
+#ifdef PCR_REFINE_CARVEOUT
+    if (warp)
+      PCR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, PCR_REFINE_CARVEOUT));
+#endif
     if (warp)
       PCR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, 0));
     else
