@@ -130,7 +130,12 @@ __global__ void materialize_kernel(const Node* __restrict__ nodes, uint32_t node
 // One warp per ray (warp_cone_walk); surviving IEs are appended with one atomic per
 // warp round.
 constexpr int kWalkThreads = 128;
-__global__ void __launch_bounds__(kWalkThreads) walk_kernel(const Ray* __restrict__ rays, uint32_t n_rays, GridView g,
+// 8 blocks of 128 threads per SM (64 registers): C3 cone walk 9.32 s at the
+// compiler's 80 registers, 9.42 s at 72, 8.89 s at 64, 9.55 s at 48 (same box)
+#ifndef PCR_WALK_MINB
+#define PCR_WALK_MINB 8
+#endif
+__global__ void __launch_bounds__(kWalkThreads, PCR_WALK_MINB) walk_kernel(const Ray* __restrict__ rays, uint32_t n_rays, GridView g,
                                                             TraceCfg c, bool filter, Task* __restrict__ tasks,
                                                             uint32_t* __restrict__ n_tasks, uint32_t cap,
                                                             unsigned long long* __restrict__ stats) {
@@ -189,7 +194,13 @@ struct SpawnOut {
 __device__ void spawn_reception(const Task tk, const Ray& r, const Node* __restrict__ parent_nodes, const GridView& g,
                                 const SceneView& s, const TraceCfg& c, SpawnOut& o);
 
-__global__ void __launch_bounds__(128, 6) visibility_kernel(const Task* __restrict__ tasks, uint32_t n_tasks,
+// 8 blocks of 128 threads per SM (64 registers; the spills stay in L1): C3
+// visibility 17.4 s at 168 registers, 13.6 s at 128, 13.4 s at 80, 12.3 s at 64
+// and 48 (same box); C2 30.9 -> 27.7 ms
+#ifndef PCR_VIS_MINB
+#define PCR_VIS_MINB 8
+#endif
+__global__ void __launch_bounds__(128, PCR_VIS_MINB) visibility_kernel(const Task* __restrict__ tasks, uint32_t n_tasks,
                                                          const Ray* __restrict__ rays,
                                                          const Node* __restrict__ parent_nodes, GridView g,
                                                          SceneView s, TraceCfg c, SpawnOut o) {
