@@ -207,12 +207,26 @@ __global__ void __launch_bounds__(128, PCR_VIS_MINB) visibility_kernel(const Tas
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  // visible tasks are queued one per lane and spawned 32 at a time (one lane each)
+  // instead of by lane 0 alone after every test; appends are atomic either way and
+  // the node/candidate order is canonicalised downstream
+  uint32_t mine = 0;
+  int queued = 0;
   for (uint32_t t = warp; t < n_tasks; t += nwarps) {
     const Task tk = tasks[t];
     const Ray r = rays[tk.ray];
     const V3 rp = ld3(g.ie_rp[tk.ie]);
     if (!warp_segment_visible(r.o, rp, tk.ie, g, s)) continue;
-    if (lane == 0) spawn_reception(tk, r, parent_nodes, g, s, c, o);
+    if (lane == queued) mine = t;
+    if (++queued == 32) {
+      const Task q = tasks[mine];
+      spawn_reception(q, rays[q.ray], parent_nodes, g, s, c, o);
+      queued = 0;
+    }
+  }
+  if (lane < queued) {
+    const Task q = tasks[mine];
+    spawn_reception(q, rays[q.ray], parent_nodes, g, s, c, o);
   }
 }
 
