@@ -3,7 +3,8 @@
 
 Workload (BASELINE.json configs[1]): synthetic indoor office,
 1,000,902 labeled points sampled with the reference's rectangle sampler, 1 TX /
-64 RX, 40 diffraction edges, max 3 interactions incl. <= 1 diffraction, every other
+64 RX, 40 diffraction edges, max 4 interactions incl. <= 1 diffraction ("3 reflections +
+1 diffraction"; SURVEY.md §8.0 fixes C2 at max_interactions 4 / max_diffractions 1), every other
 RunConfig field at the paper's Table-1 defaults. A step is one full pass of the hot
 path over the scene: validate -> voxelize -> transmission + propagation -> refinement
 -> dedup (run_pipeline_on_scene semantics, outputs identical to the reference).
@@ -123,11 +124,13 @@ def measured_traffic(kernel):
         return None
 
 
-def roofline(kernel, ms_total, launches, summary, mean_depth, peaks, peaks_kind, fp64_tflops):
+def roofline(kernel, ms_total, launches, summary, peaks, peaks_kind, fp64_tflops):
     if kernel == "refine":
-        flops = (summary["refine_trials"] * (FLOP_TRIAL_PER_NODE * mean_depth + FLOP_TRIAL_BASE)
+        # per-path node counts weight the per-node terms (counted by the kernel:
+        # refine_trial_nodes = sum over trials of d, refine_iter_nodes = sum over iterations of d)
+        flops = (summary["refine_trial_nodes"] * FLOP_TRIAL_PER_NODE + summary["refine_trials"] * FLOP_TRIAL_BASE
                  + summary["refine_marches"] * FLOP_MARCH
-                 + summary["refine_iterations"] * mean_depth * FLOP_ITER_PER_NODE)
+                 + summary["refine_iter_nodes"] * FLOP_ITER_PER_NODE)
         per_launch = flops / max(launches, 1)
         achieved = per_launch / (ms_total / max(launches, 1) * 1e-3) / 1e12
         return {"bound": "fp64", "kernel": kernel, "achieved": achieved, "peak": fp64_tflops, "unit": "TFLOP/s",
@@ -315,9 +318,7 @@ def b200_arm(args, rank, world, local_rank):
     peaks, peaks_kind = measured_peaks()
     fp64 = pcray.fp64_probe(ctx)
     dom = max(ktimes.items(), key=lambda kv: kv[1][0]) if ktimes else ("none", (0.0, 1))
-    mean_depth = 3.0
-    rl = roofline(dom[0], dom[1][0] / args.steps, max(1, dom[1][1] // args.steps), own, mean_depth, peaks,
-                  peaks_kind, fp64)
+    rl = roofline(dom[0], dom[1][0] / args.steps, max(1, dom[1][1] // args.steps), own, peaks, peaks_kind, fp64)
     total_k = sum(v[0] for v in ktimes.values())
     shares = {k: round(v[0] / total_k, 4) for k, v in sorted(ktimes.items(), key=lambda kv: -kv[1][0])}
 
@@ -353,6 +354,9 @@ def b200_arm(args, rank, world, local_rank):
             # Mrays/s over the trace stage alone (R / t_trace), beside `value` (R / step)
             "mrays_per_s_trace": rays / dict(s0["timings"]).get("trace", float("nan")) / 1e6,
             "exact_paths": s0["exact_paths"], "coarse_paths": s0["coarse_paths"],
+            # knife-edge atan2/asin cone decisions not certified against glibc (trace.cuh libm_le): 0
+            # means every cone decision of the step is the reference's
+            "libm_unresolved": s0.get("libm_unresolved") if rank == 0 else None,
             "stage_seconds": dict(s0["timings"]), "kernel_share": shares,
             "roofline": rl,
             "cpu_baseline": cpu,

@@ -200,6 +200,9 @@ typedef struct pcr_summary {
   uint64_t refine_marches;    /* march_segment / projection calls inside reproject */
   uint64_t walk_cells;        /* cells evaluated by cone walks (neighbourhood scans) */
   uint64_t walk_ies;          /* IE records tested by cone walks */
+  uint64_t libm_unresolved;   /* knife-edge atan2/asin decisions not certified vs glibc (trace.cuh libm_le) */
+  uint64_t refine_trial_nodes; /* sum over trials of the path's node count (flop model) */
+  uint64_t refine_iter_nodes;  /* sum over iterations of the path's node count (flop model) */
 } pcr_summary;
 
 /* A conical ray (tracer.hpp:40-47) for the batch primitives; planes are given
@@ -267,6 +270,11 @@ int pcr_transmission_phase(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* 
 int pcr_propagate(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene, uint32_t tx_index,
                   const pcr_initial_hits* hits, const pcr_trace_params* params,
                   pcr_paths** out);
+/* work counters of the last pcr_propagate on this context: [0] voxel_cone_trace
+ * invocations (= the reference's dfs_trace calls, tracer.cpp:420), [1] visibility
+ * tests, [2] cells and [3] IE records the cone walk read (SURVEY 8d units), [4]
+ * knife-edge atan2/asin decisions not certified against glibc (expected 0) */
+int pcr_last_trace_stats(pcr_ctx* ctx, uint64_t* out5);
 /* voxel_cone_trace (tracer.hpp:118-120; tracer.cpp:313-403) over a batch of rays */
 int pcr_cone_trace_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene,
                          const pcr_ray_desc* rays, uint64_t n_rays, int want_debug,
@@ -358,6 +366,7 @@ int pcr_run_pipeline(pcr_ctx* ctx, const pcr_run_files* files, const pcr_run_con
 typedef struct pcr_shard_stats {
   uint64_t cone_traces, visibility_tests, walk_cells, walk_ies; /* propagation of the shard */
   uint64_t refine_iterations, refine_trials, refine_marches;    /* refinement of the shard */
+  uint64_t libm_unresolved, refine_trial_nodes, refine_iter_nodes;
 } pcr_shard_stats;
 int pcr_shard_trace(pcr_ctx* ctx, const pcr_scene* scene, const pcr_run_config* config, uint32_t shard,
                     uint32_t n_shards, uint64_t* n_rows, uint64_t* row_bytes);

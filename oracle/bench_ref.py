@@ -75,10 +75,13 @@ def run_sample(scene, run: dict, stride: int = 1, threads: int = 0):
         n_hits += sub["n"]
         parts += [los, ref.propagate(grid, rs, t, sub, tp, thread_count=threads)]
     cands = concat_paths(parts)
-    out = ref.refine_batch(grid, rs, cands, rp, thread_count=threads) if cands["n"] else {"has_path": np.zeros(0)}
+    # refine_path + the pipeline's dedup: "exact" counts what RunSummary::exact_paths counts
+    # (pipeline.cpp:181-208), the same definition as the GPU arm's exact_paths
+    exact = ref.refine_dedup_count(grid, rs, cands, rp, thread_count=threads,
+                                   carrier_frequency_hz=cfg.carrier_frequency_hz) if cands["n"] else 0
     seconds = time.perf_counter() - t0
     n_ies = len(grid.to_dict()["ie_kind"])
-    return {"seconds": seconds, "candidates": int(cands["n"]), "exact": int(np.sum(out["has_path"])),
+    return {"seconds": seconds, "candidates": int(cands["n"]), "exact": int(exact),
             "transmission_rays": n_ies * n_tx, "initial_hits_traced": n_hits, "stride": stride}
 
 

@@ -102,6 +102,8 @@ def _load(path):
         L.pcrref_refine_batch.argtypes = [vp, vp, pp(abi.Paths), pp(abi.RefineParams), C.c_int,
                                           pp(pp(abi.Outcomes))]
         L.pcrref_free_outcomes.argtypes = [pp(abi.Outcomes)]
+        L.pcrref_refine_dedup_batch.argtypes = [vp, vp, pp(abi.Paths), pp(abi.RefineParams), C.c_int, C.c_double,
+                                                pp(C.c_uint64), pp(pp(abi.Outcomes))]
         L.pcrref_run_pipeline_on_scene.argtypes = [vp, pp(abi.RunConfig), pp(pp(abi.Summary))]
         L.pcrref_free_summary.argtypes = [pp(abi.Summary)]
         L.pcrref_free_paths.argtypes = [pp(abi.Paths)]
@@ -270,6 +272,18 @@ def refine_batch(grid: RefGrid, scene: RefScene, candidates: dict, params=None, 
         return abi.outcomes_to_dict(out.contents)
     finally:
         lib().pcrref_free_outcomes(out)
+
+
+def refine_dedup_count(grid: RefGrid, scene: RefScene, candidates: dict, params=None, thread_count=0,
+                       carrier_frequency_hz=60e9) -> int:
+    """refine_path on every candidate, then the pipeline's dedup_by_label ->
+    dedup_by_fresnel (pipeline.cpp:181-208): the number RunSummary::exact_paths counts."""
+    params = params or abi.refine_params()
+    keep = abi.PathsKeepAlive(candidates)
+    n = C.c_uint64()
+    _check(lib().pcrref_refine_dedup_batch(grid.handle, scene.handle, C.byref(keep.paths), C.byref(params),
+                                           thread_count, carrier_frequency_hz, C.byref(n), None))
+    return int(n.value)
 
 
 def run_pipeline_on_scene(scene: RefScene, config: abi.RunConfig | None = None):

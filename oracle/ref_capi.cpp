@@ -7,6 +7,7 @@
 // Nothing in the product (paper_2402_13747_b200/) links, loads or calls this.
 // Every function forwards to the reference entry point cited beside it.
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -526,8 +527,9 @@ int pcrref_march_segment_batch(const void* grid, const void* scene, const double
 // ---- stage 3 -------------------------------------------------------------------
 // refine_path (refine.cpp:189-286) per candidate; LOS rows pass through as in
 // run_pipeline_on_scene (pipeline.cpp:160-170).
-int pcrref_refine_batch(const void* grid, const void* scene, const pcr_paths* cands,
-                        const pcr_refine_params* rp, int thread_count, pcr_outcomes** out) {
+static int refine_batch_impl(const void* grid, const void* scene, const pcr_paths* cands,
+                             const pcr_refine_params* rp, int thread_count, pcr_outcomes** out,
+                             double carrier_frequency_hz, uint64_t* n_dedup) {
   return guarded([&] {
     const VoxelGrid& g = *static_cast<const VoxelGrid*>(grid);
     const Scene& s = *static_cast<const Scene*>(scene);
@@ -553,6 +555,22 @@ int pcrref_refine_batch(const void* grid, const void* scene, const pcr_paths* ca
         oc[i] = refine_path(cv[i], g, s, p);
       }
     });
+    if (n_dedup) {
+      // the pipeline's post-refine step (pipeline.cpp:181-208): exact paths, then
+      // dedup_by_label -> dedup_by_fresnel (refine.cpp:324-372) -> final sort
+      std::vector<ExactPath> exact;
+      for (const RefineOutcome& r : oc)
+        if (r.path) exact.push_back(*r.path);
+      exact = dedup_by_label(std::move(exact));
+      if (p.fresnel_enabled) exact = dedup_by_fresnel(std::move(exact), carrier_frequency_hz);
+      std::sort(exact.begin(), exact.end(), [](const ExactPath& a, const ExactPath& b) {
+        if (a.tx_id != b.tx_id) return a.tx_id < b.tx_id;
+        if (a.rx_id != b.rx_id) return a.rx_id < b.rx_id;
+        return a.delay < b.delay;
+      });
+      *n_dedup = exact.size();
+    }
+    if (!out) return;
     pcr_outcomes* o = alloc<pcr_outcomes>(1);
     pcr_paths* pp = alloc_paths(cv.size(), std::max<std::uint32_t>(1, cands->stride));
     o->paths = *pp;
@@ -566,6 +584,19 @@ int pcrref_refine_batch(const void* grid, const void* scene, const pcr_paths* ca
     }
     *out = o;
   });
+}
+
+int pcrref_refine_batch(const void* grid, const void* scene, const pcr_paths* cands,
+                        const pcr_refine_params* rp, int thread_count, pcr_outcomes** out) {
+  return refine_batch_impl(grid, scene, cands, rp, thread_count, out, 0.0, nullptr);
+}
+
+// refine_path per candidate + the pipeline's dedup (bench CPU arm: exact paths counted
+// the way RunSummary::exact_paths counts them); outcomes optional (out may be null)
+int pcrref_refine_dedup_batch(const void* grid, const void* scene, const pcr_paths* cands,
+                              const pcr_refine_params* rp, int thread_count, double carrier_frequency_hz,
+                              uint64_t* n_exact, pcr_outcomes** out) {
+  return refine_batch_impl(grid, scene, cands, rp, thread_count, out, carrier_frequency_hz, n_exact);
 }
 
 void pcrref_free_outcomes(pcr_outcomes* o) {

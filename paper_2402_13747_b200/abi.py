@@ -101,7 +101,8 @@ class Summary(C.Structure):
         ("hash", C.c_uint64), ("paths", Paths), ("transmission_rays", C.c_uint64),
         ("cone_traces", C.c_uint64), ("visibility_tests", C.c_uint64), ("refine_iterations", C.c_uint64),
         ("refine_trials", C.c_uint64), ("refine_marches", C.c_uint64), ("walk_cells", C.c_uint64),
-        ("walk_ies", C.c_uint64),
+        ("walk_ies", C.c_uint64), ("libm_unresolved", C.c_uint64), ("refine_trial_nodes", C.c_uint64),
+        ("refine_iter_nodes", C.c_uint64),
     ]
 
 
@@ -137,7 +138,8 @@ class RunFilesKeepAlive:
 
 
 SHARD_STATS_FIELDS = ("cone_traces", "visibility_tests", "walk_cells", "walk_ies", "refine_iterations",
-                      "refine_trials", "refine_marches")
+                      "refine_trials", "refine_marches", "libm_unresolved", "refine_trial_nodes",
+                      "refine_iter_nodes")
 
 
 class ShardStats(C.Structure):
@@ -342,7 +344,8 @@ def summary_to_dict(s: Summary) -> dict:
         "transmission_rays": int(s.transmission_rays), "cone_traces": int(s.cone_traces),
         "visibility_tests": int(s.visibility_tests), "refine_iterations": int(s.refine_iterations),
         "refine_trials": int(s.refine_trials), "refine_marches": int(s.refine_marches),
-        "walk_cells": int(s.walk_cells), "walk_ies": int(s.walk_ies),
+        "walk_cells": int(s.walk_cells), "walk_ies": int(s.walk_ies), "libm_unresolved": int(s.libm_unresolved),
+        "refine_trial_nodes": int(s.refine_trial_nodes), "refine_iter_nodes": int(s.refine_iter_nodes),
     }
 
 

@@ -306,6 +306,14 @@ int pcr_propagate(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene, ui
   });
 }
 
+int pcr_last_trace_stats(pcr_ctx* ctx, uint64_t* out5) {
+  return guarded(ctx, [&] {
+    uint64_t* out4 = out5;
+    if (!out4) throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    for (int i = 0; i < 5; ++i) out4[i] = ctx->c.last_trace[i];
+  });
+}
+
 int pcr_cone_trace_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene, const pcr_ray_desc* rays,
                          uint64_t n_rays, int want_debug, pcr_receptions** out) {
   return guarded(ctx, [&] {

@@ -131,6 +131,8 @@ struct Ctx {
   int fan_n = 0;
   DBuf<double> fan_table;  // n*6: cos phi, sin phi, sin(phi+dphi/2), cos(phi+dphi/2), sin(phi-dphi/2), cos(phi-dphi/2)
   int sm_count = 148;
+  // work counters of the last pcr_propagate call (cone traces, visibility tests, cells, IEs)
+  uint64_t last_trace[5] = {0, 0, 0, 0, 0};
   // per-kernel CUDA-event timing (pcr_set_profiling); resolved lazily
   bool profiling = false;
   struct Pending {

@@ -949,6 +949,7 @@ void run_pipeline_core(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cf
     S->cone_traces = st.cone_traces;
     S->walk_cells = st.walk_cells;
     S->walk_ies = st.walk_ies;
+    S->libm_unresolved = st.libm_unresolved;
     S->visibility_tests += st.visibility_tests;
     assemble_cands(ctx, scene, grid, txs, slices, stride_of(cfg), cs);
   } catch (const std::exception& e) {
@@ -964,6 +965,8 @@ void run_pipeline_core(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cf
     refine_cands(ctx, grid, scene, cs, cfg, 0, 1, ro);
     S->refine_trials = ro.trials;
     S->refine_marches = ro.marches;
+    S->refine_trial_nodes = ro.trial_nodes;
+    S->refine_iter_nodes = ro.iter_nodes;
   } catch (const std::exception& e) {
     stage_fail("refine", e);
   }
@@ -1114,6 +1117,7 @@ void api_shard_trace(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg,
     st.stats.visibility_tests = ts.visibility_tests;
     st.stats.walk_cells = ts.walk_cells;
     st.stats.walk_ies = ts.walk_ies;
+    st.stats.libm_unresolved = ts.libm_unresolved;
     const size_t bytes = cand_row_bytes(stride);
     st.rows.alloc(total ? total * bytes : 1, s);
     uint64_t row = 0;
@@ -1170,6 +1174,8 @@ void api_shard_refine(Ctx& ctx, const SceneDev& scene, const void* rows, uint64_
     refine_cands(ctx, st.grid, scene, st.cs, st.cfg, st.shard, st.n_shards, ro);
     st.stats.refine_trials = ro.trials;
     st.stats.refine_marches = ro.marches;
+    st.stats.refine_trial_nodes = ro.trial_nodes;
+    st.stats.refine_iter_nodes = ro.iter_nodes;
     const uint32_t n = st.cs.n;
     const uint32_t n_sub = n > st.shard ? (n - st.shard + st.n_shards - 1) / st.n_shards : 0;
     const size_t bytes = out_row_bytes(stride);
@@ -1223,6 +1229,9 @@ void api_shard_finish(Ctx& ctx, const void* rows, uint64_t n_rows, const pcr_sha
   S->cone_traces = totals.cone_traces;
   S->walk_cells = totals.walk_cells;
   S->walk_ies = totals.walk_ies;
+  S->libm_unresolved = totals.libm_unresolved;
+  S->refine_trial_nodes = totals.refine_trial_nodes;
+  S->refine_iter_nodes = totals.refine_iter_nodes;
   S->visibility_tests += totals.visibility_tests;
   S->refine_trials = totals.refine_trials;
   S->refine_marches = totals.refine_marches;

@@ -305,7 +305,7 @@ struct RefOut {
   double* delay;
   double* gnorm;
   uint32_t* iters;
-  unsigned long long* stats;  // [0] trials, [1] reprojection marches
+  unsigned long long* stats;  // [0] trials, [1] reprojection marches, [2] trial nodes, [3] iteration nodes
 };
 
 // Dynamic state of a path between iterations: reflection nodes are (c, normal,
@@ -443,9 +443,12 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
   bool converged = false;
   int iter = 0;
   uint32_t n_trials = 0, n_march = 0;
+  uint64_t n_iter_nodes = 0;
   auto flush = [&]() {
     atomicAdd(o.stats, static_cast<unsigned long long>(n_trials));
     atomicAdd(o.stats + 1, static_cast<unsigned long long>(n_march));
+    atomicAdd(o.stats + 2, static_cast<unsigned long long>(n_trials) * d);
+    atomicAdd(o.stats + 3, static_cast<unsigned long long>(n_iter_nodes));
   };
   // Brent cycle detection on the post-iteration state
   Snapshot<D> saved, last[2];  // Brent's saved state; the states 1 and 2 iterations back
@@ -455,6 +458,7 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
   int power = 1, lam = 0;
   bool stalled = false;
   for (; iter < rho; ++iter) {
+    n_iter_nodes += d;
     // local_gradients
     double gr[2 * D];
     int ng = 0;
@@ -725,7 +729,8 @@ __device__ PCR_STEP_INLINE void path_converged(const PathState<D>& st, const Can
 // convergence test, backtracking (:209-232). False when the path is finished.
 template <int D>
 __device__ PCR_STEP_INLINE bool path_step_a(PathState<D>& st, const CandIn& in, const GridView& g, const SceneView& s, double delta,
-                            int rho, double step_size, const RefOut& o, uint32_t& n_trials) {
+                            int rho, double step_size, const RefOut& o, uint32_t& n_trials,
+                            unsigned long long& n_nodes) {
   const uint32_t k = st.k;
   const int d = st.d;
   if (st.iter >= rho) {
@@ -735,6 +740,7 @@ __device__ PCR_STEP_INLINE bool path_step_a(PathState<D>& st, const CandIn& in, 
   }
   // loops unrolled to the depth bound with q < d guards: the per-node values stay in
   // registers (a runtime-indexed array would live in local memory)
+  n_nodes += static_cast<unsigned long long>(d) << 32;  // iteration executed (high word)
   double ga[D], gb[D];
   bool refl[D];
   V3 pts[D];
@@ -799,6 +805,7 @@ __device__ PCR_STEP_INLINE bool path_step_a(PathState<D>& st, const CandIn& in, 
       }
     }
     ++n_trials;
+    n_nodes += static_cast<unsigned long long>(d);  // trial nodes (low word)
     if (len + norm(st.rx - prev) <= st.f + 1e-15) {
 #pragma unroll
       for (int q = 0; q < D; ++q) {
@@ -1029,6 +1036,7 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
   PathState<D> st;
   bool active = false, open = true;
   uint32_t n_trials = 0, n_march = 0;
+  unsigned long long n_nodes = 0;  // per lane: iteration nodes << 32 | trial nodes
   ScanCache cache{0x7ff8dead7ff8deadll, 0x7ff8dead7ff8deadll, 0.0, 0u};
   uint32_t done = 0;
   unsigned long long t_start = 0, t_last = 0;
@@ -1043,7 +1051,7 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
       active = path_init(st, in.first + idx * in.step, in, s, o);
     }
     if (!__any_sync(kFull, active)) break;
-    bool alive = active && path_step_a(st, in, g, s, delta, rho, step_size, o, n_trials);
+    bool alive = active && path_step_a(st, in, g, s, delta, rho, step_size, o, n_trials, n_nodes);
     // reprojection, front to back (refine.cpp:234-250), node index by node index
     for (int q = 0; q < D; ++q) {
       bool need = alive && q < st.d && st.nd[q].kind == 0;
@@ -1123,6 +1131,8 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
   }
   atomicAdd(o.stats, static_cast<unsigned long long>(n_trials));
   atomicAdd(o.stats + 1, static_cast<unsigned long long>(n_march + cache.n_march));
+  atomicAdd(o.stats + 2, n_nodes & 0xffffffffull);
+  atomicAdd(o.stats + 3, n_nodes >> 32);
 }
 
 // 3 blocks of 128 threads per SM (168 registers): measured 4 -> 873 ms, 3 -> 686 ms,
@@ -1303,10 +1313,10 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     gv.nb_pb = nb_pb.get();
   }
   CandIn ci{in.first, step, in.stride, in.tx, in.rx, in.n_inter, in.kind, in.pos, in.label, in.nrm, in.edge, in.coarse_length};
-  DBuf<unsigned long long> stats(2, s);
+  DBuf<unsigned long long> stats(4, s);
   DBuf<uint32_t> next(1, s);
   PCR_CUDA(cudaMemsetAsync(next.get(), 0, sizeof(uint32_t), s));
-  PCR_CUDA(cudaMemsetAsync(stats.get(), 0, 2 * sizeof(unsigned long long), s));
+  PCR_CUDA(cudaMemsetAsync(stats.get(), 0, 4 * sizeof(unsigned long long), s));
   RefOut ro{out.reason.get(), out.has_path.get(), out.pos.get(), out.nrm.get(), out.label.get(),
             out.length.get(), out.delay.get(), out.gnorm.get(), out.iters.get(), stats.get()};
   count_launch();
@@ -1382,11 +1392,13 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     }
   }
   PCR_LAUNCH_CHECK();
-  unsigned long long hs[2];
-  d2h(hs, stats.get(), 2, s);
+  unsigned long long hs[4];
+  d2h(hs, stats.get(), 4, s);
   PCR_CUDA(cudaStreamSynchronize(s));
   out.trials = hs[0];
   out.marches = hs[1];
+  out.trial_nodes = hs[2];
+  out.iter_nodes = hs[3];
 }
 
 void api_refine_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const pcr_paths& c,

@@ -21,6 +21,7 @@ struct TxDev {
 // Work counters of a propagate call (SURVEY §8d units).
 struct TraceStats {
   uint64_t cone_traces = 0, visibility_tests = 0, walk_cells = 0, walk_ies = 0;
+  uint64_t libm_unresolved = 0;  // knife-edge atan2/asin decisions not certified (trace.cuh libm_le)
 };
 
 // Kept propagation candidates of one TX in output (DFS) order; interaction
@@ -49,6 +50,7 @@ struct RefineDevOut {
   DBuf<double> pos, nrm, length, delay, gnorm;
   DBuf<uint32_t> label, iters;
   uint64_t trials = 0, marches = 0;  // work counters (summed over candidates)
+  uint64_t trial_nodes = 0, iter_nodes = 0;  // the same weighted by the path's node count
 };
 
 void transmission_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint32_t tx_index, TxDev& out);

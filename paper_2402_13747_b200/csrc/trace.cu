@@ -56,7 +56,7 @@ __device__ __forceinline__ bool fan_frame(const double* edge, const V3& incoming
   w = normalized(e - s);
   cos_b = dot(incoming, w);
   if (fabs(cos_b) > 0.999) return false;
-  if (angle_between(na, nb) <= 1e-9) return false;
+  if (libm_le(angle_between(na, nb), 1e-9, 4.0)) return false;  // atan2: see libm_le
   if (dot(incoming, na) >= 0.0 && dot(incoming, nb) >= 0.0) return false;
   e1 = safe_normalized(incoming - cos_b * w);
   if (is_zero(e1)) return false;
@@ -938,6 +938,10 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
   DBuf<unsigned long long> alive(1, s);
   DBuf<unsigned long long> walk_stats(2, s);
   PCR_CUDA(cudaMemsetAsync(walk_stats.get(), 0, 2 * sizeof(unsigned long long), s));
+  {
+    const unsigned long long zero = 0;
+    PCR_CUDA(cudaMemcpyToSymbolAsync(g_libm_unresolved, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, s));
+  }
 
   std::vector<StackEntry> stack;
   auto push_range = [&](uint32_t begin, uint32_t count) {
@@ -1079,11 +1083,13 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
                                                    co);
     PCR_LAUNCH_CHECK();
   }
-  unsigned long long ws[2] = {0, 0};
+  unsigned long long ws[2] = {0, 0}, unresolved = 0;
   d2h(ws, walk_stats.get(), 2, s);
+  PCR_CUDA(cudaMemcpyFromSymbolAsync(&unresolved, g_libm_unresolved, sizeof(unresolved), 0, cudaMemcpyDeviceToHost, s));
   PCR_CUDA(cudaStreamSynchronize(s));
   stats.walk_cells += ws[0];
   stats.walk_ies += ws[1];
+  stats.libm_unresolved += unresolved;
 }
 
 // ---- sharded propagation: candidate rows and the global kappa merge ---------
@@ -1398,6 +1404,11 @@ void api_propagate(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint32_
   TraceStats st;
   propagate_device(ctx, grid, scene, tx_index, ie.get(), kind.get(), pos.get(), nrm.get(), inc.get(),
                    static_cast<uint32_t>(n), p, cd, st);
+  ctx.last_trace[0] = st.cone_traces;
+  ctx.last_trace[1] = st.visibility_tests;
+  ctx.last_trace[2] = st.walk_cells;
+  ctx.last_trace[3] = st.walk_ies;
+  ctx.last_trace[4] = st.libm_unresolved;
   pcr_paths* r = alloc_paths(cd.n, cd.stride);
   fill_paths_from_cands(cd, scene.h_tx_id[tx_index], &scene.h_tx[3ull * tx_index], r, 0, s);
   *out = r;

@@ -142,6 +142,27 @@ __device__ __forceinline__ void cone_walk(const GridView& g, const Ray& r, OnEva
   if (n_ies) *n_ies += ies_seen;
 }
 
+// Knife-edge libm decisions. The reference decides `atan2(..) <= alpha +
+// asin(..)` (tracer.cpp:129-136, geometry.hpp:33-37) and `angle_between(na, nb) <=
+// 1e-9` (tracer.cpp:275-284) with glibc; the device evaluates the same expressions
+// with CUDA's libm. Both libms are within a few ulp of the exact values (glibc < 1 ulp,
+// CUDA atan2/asin <= 2 ulp), so whenever the two sides differ by more than `ulps`
+// units in the last place of the larger one the decision is the reference's; a
+// comparison inside that margin is counted here (read per propagate call into
+// TraceStats::libm_unresolved, reported in the RunSummary counters, asserted zero by
+// the contract tests) — a run with a zero count is bit-exact in every such decision.
+static __device__ unsigned long long g_libm_unresolved = 0;
+__device__ __forceinline__ double ulp_of(double x) {
+  const long long e = __double_as_longlong(fabs(x)) & 0x7ff0000000000000ll;
+  return e ? __longlong_as_double(e) * 2.220446049250313e-16 : 4.9406564584124654e-324;
+}
+__device__ __forceinline__ bool libm_le(double a, double b, double ulps) {
+  const double m = fabs(a - b);
+  const double sc = fabs(a) < fabs(b) ? fabs(b) : fabs(a);
+  if (!(m > ulps * ulp_of(sc))) atomicAdd(&g_libm_unresolved, 1ull);
+  return a <= b;
+}
+
 // cone_intersects_sphere (tracer.cpp:129-136) with an exact-equivalent fast path.
 // beta = atan2(|vc x d|, vc.d) <= rhs = alpha + asin(min(1, r/dist)) is, on [0, pi],
 // cos(beta) >= cos(rhs) with cos(beta) = vc.d / (|vc||d|) and
@@ -175,8 +196,10 @@ __device__ __forceinline__ bool cone_test(const V3& o, const V3& d, const ConeCo
     if (diff > 1e-9) return true;
     if (diff < -1e-9) return false;
   }
+  // the band: the reference's expression; atan2 and asin each within 3 ulp of glibc's
+  // and one rounding of the sum -> 8 ulp of [0, pi] values certify the outcome
   const double beta = angle_between(vc, d);
-  return beta <= k.alpha + asin(smin(1.0, r / dist));
+  return libm_le(beta, k.alpha + asin(smin(1.0, r / dist)), 8.0);
 }
 
 // Warp-cooperative voxel_cone_trace walk: the 32 lanes hold the same ray, walker

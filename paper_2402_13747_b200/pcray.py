@@ -56,6 +56,7 @@ def lib():
                                              pp(pp(abi.InitialHits))]
         L.pcr_propagate.argtypes = [vp, vp, vp, C.c_uint32, pp(abi.InitialHits), pp(abi.TraceParams),
                                     pp(pp(abi.Paths))]
+        L.pcr_last_trace_stats.argtypes = [vp, pp(C.c_uint64)]
         L.pcr_cone_trace_batch.argtypes = [vp, vp, vp, pp(abi.RayDesc), C.c_uint64, C.c_int,
                                            pp(pp(abi.Receptions))]
         L.pcr_segment_visible_batch.argtypes = [vp, vp, vp, pp(C.c_double), pp(C.c_double), pp(C.c_uint32),
@@ -106,7 +107,7 @@ EXPORTED_SYMBOLS = [
     "pcr_free_summary", "pcr_free_receptions", "pcr_run_pipeline_device", "pcr_shard_trace", "pcr_shard_rows",
     "pcr_shard_refine", "pcr_shard_outcomes", "pcr_shard_stats_get", "pcr_shard_finish", "pcr_scene_load_ply",
     "pcr_scene_points", "pcr_write_paths", "pcr_libm_exp_batch", "pcr_load_edges", "pcr_free_edges",
-    "pcr_run_pipeline",
+    "pcr_run_pipeline", "pcr_last_trace_stats",
 ]
 
 
@@ -268,6 +269,16 @@ def propagate(tx_index: int, hits: dict, grid: DeviceGrid, scene: DeviceScene, p
         return abi.paths_to_dict(out.contents)
     finally:
         lib().pcr_free_paths(out)
+
+
+def last_trace_stats(ctx: Context | None = None) -> dict:
+    """Work counters of the last propagate on ctx (cone traces = the reference's
+    voxel_cone_trace / dfs_trace calls, visibility tests, cells and IEs walked)."""
+    ctx = ctx or Context.default()
+    a = (C.c_uint64 * 5)()
+    ctx.check(lib().pcr_last_trace_stats(ctx.handle, a))
+    return dict(zip(["cone_traces", "visibility_tests", "walk_cells", "walk_ies", "libm_unresolved"],
+                    (int(x) for x in a)))
 
 
 def make_ray(origin, direction, apex_angle, planes=(), origin_ie=abi.NO_IE, origin_label=0) -> abi.RayDesc:

@@ -267,17 +267,22 @@ def config(name: str) -> SceneConfig:
         return SceneConfig("C1", p, 1700.0, 7, dict(max_interactions=2, max_diffractions=0),
                            "synthetic labeled box room, 100k points, 1 TX / 1 RX, max 2 reflections")
     if name == "C2":
-        return SceneConfig("C2", office_planar(), 1545.0, 11, dict(max_interactions=3, max_diffractions=1),
-                           "synthetic indoor office, 1M points, 1 TX / 64 RX, 3 interactions incl. <= 1 diffraction")
+        # "3 reflections + 1 diffraction" = 4 interactions; the reference caps only the
+        # total and the diffraction count (tracer.cpp:418-472), SURVEY.md §8.0
+        return SceneConfig("C2", office_planar(), 1545.0, 11, dict(max_interactions=4, max_diffractions=1),
+                           "synthetic indoor office, 1M points, 1 TX / 64 RX, 4 interactions incl. <= 1 diffraction")
+    if name == "C2d3":
+        return SceneConfig("C2d3", office_planar(), 1545.0, 11, dict(max_interactions=3, max_diffractions=1),
+                           "C2 at depth 3 (secondary, shallower than the contract's 4 / 1)")
     if name == "C2np":
-        return SceneConfig("C2np", office_planar(), 1545.0, 11, dict(max_interactions=3, max_diffractions=1),
+        return SceneConfig("C2np", office_planar(), 1545.0, 11, dict(max_interactions=4, max_diffractions=1),
                            "C2 with every normal tilted by up to 1 deg (seeded): non-planar IEs, exp() SDF path")
     if name == "C3":
         return SceneConfig("C3", canyon_planar(), 625.0, 3, dict(max_interactions=3, max_diffractions=0),
                            "synthetic street canyon, 10M points, 4 TX / 256 RX, 3 reflections")
     if name == "C4":
-        return SceneConfig("C4", dense_floor_planar(), 1950.0, 5, dict(max_interactions=4, max_diffractions=1),
-                           "dense synthetic floor, 10M points, 16 TX / 1024 RX, 4 interactions incl. <= 1 diffraction")
+        return SceneConfig("C4", dense_floor_planar(), 1950.0, 5, dict(max_interactions=5, max_diffractions=1),
+                           "dense synthetic floor, 10M points, 16 TX / 1024 RX, 5 interactions incl. <= 1 diffraction")
     raise KeyError(name)
 
 

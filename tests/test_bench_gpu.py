@@ -16,6 +16,14 @@ KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "
         "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"}
 
 
+def _golden_c2():
+    """The bench workload's counts as the oracle computes them on the full scene
+    (tests/golden/make_contract_golden.py)."""
+    with open(os.path.join(ROOT, "tests", "golden", "contract_C2.json")) as f:
+        g = json.load(f)
+    return g["summary"]["exact_paths"], g["summary"]["coarse_paths"], g["cone_traces"] + g["transmission_rays"]
+
+
 def _last_json(out):
     return json.loads([l for l in out.splitlines() if l.startswith("{")][-1])
 
@@ -28,7 +36,9 @@ def test_bench_single_gpu_line():
     assert KEYS <= set(line)
     assert line["n_gpus"] == 1 and line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
     assert line["roofline"]["kernel"] == "refine" and 0 < line["roofline"]["frac"] < 1
-    assert line["exact_paths"] == 13716 and line["coarse_paths"] == 170894  # C2, as the oracle counts
+    exact, coarse, rays = _golden_c2()
+    assert line["config"]["max_interactions"] == 4 and line["config"]["max_diffractions"] == 1
+    assert line["exact_paths"] == exact and line["coarse_paths"] == coarse and line["rays_per_step"] == rays
 
 
 def test_bench_two_ranks_gloo():
@@ -42,4 +52,5 @@ def test_bench_two_ranks_gloo():
     assert r.returncode == 0, r.stderr[-2000:]
     line = _last_json(r.stdout)
     assert KEYS <= set(line)
-    assert line["n_gpus"] == 2 and line["exact_paths"] == 13716 and line["coarse_paths"] == 170894
+    exact, coarse, rays = _golden_c2()
+    assert line["n_gpus"] == 2 and line["exact_paths"] == exact and line["coarse_paths"] == coarse

@@ -139,3 +139,35 @@ def test_restated_voxelization_matches_reference(oracle, name):
         ref = oracle.build_grid(oracle.RefScene(scene), abi.voxel_params(vs, dv)).to_dict()
         got = restate_vox.build_grid(scene, vs, dv)
         assert_grid_equal(got, ref)
+
+
+@pytest.mark.parametrize("name,run", [("C1", None), ("C2", dict(max_interactions=2, max_diffractions=1))])
+def test_cpu_arm_counts_exact_paths_after_dedup(oracle, name, run):
+    """bench.py's CPU arm counts exact paths the way RunSummary::exact_paths does
+    (refine_path, then dedup_by_label -> dedup_by_fresnel, pipeline.cpp:181-208): at
+    task stride 1 its count equals the reference pipeline's own summary."""
+    from oracle import bench_ref
+
+    scene, cfg = scenes.build_scene(name)
+    run = run or cfg.run
+    r = bench_ref.run_sample(scene, run, stride=1)
+    s = oracle.run_pipeline_on_scene(oracle.RefScene(scene), oracle.default_run_config(**run))
+    assert r["candidates"] == s["coarse_paths"]
+    assert r["exact"] == s["exact_paths"] < s["refined_paths"]
+
+
+def test_contract_goldens_match_scene_configs():
+    """The golden digests (tests/golden/make_contract_golden.py) were made for the
+    configs scenes.py defines (C2 at 4 / 1)."""
+    import json
+    import os
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    for name in ["C1", "C2d3", "C2"]:
+        p = os.path.join(here, f"contract_{name}.json")
+        if not os.path.exists(p):
+            continue
+        g = json.load(open(p))
+        assert g["run"] == scenes.config(name).run
+    assert scenes.config("C2").run == dict(max_interactions=4, max_diffractions=1)
+    assert scenes.config("C4").run == dict(max_interactions=5, max_diffractions=1)
