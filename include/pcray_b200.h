@@ -231,6 +231,8 @@ typedef struct pcr_receptions {
   double* hit_distance;
   uint64_t* evaluated_offset; /* n_rays+1 (debug: TraceDebug::evaluated, order-free) */
   uint32_t* evaluated;        /* cell indices */
+  uint64_t* visited_offset;   /* n_rays+1 (debug: TraceDebug::visited, walk order) */
+  uint32_t* visited;          /* cell indices */
 } pcr_receptions;
 
 typedef struct pcr_ctx pcr_ctx;
@@ -283,6 +285,57 @@ int pcr_cone_trace_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* sc
 int pcr_segment_visible_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene,
                               const double* origin, const double* target,
                               const uint32_t* target_ie, uint64_t n, uint8_t* visible_out);
+
+/* ---- the reference's scalar helpers as device batches (C++ drop-in, adapter/) -------
+ * Each runs the same device function the stage kernels use, one thread per item;
+ * arrays are host memory, n items each (vectors as n*3). */
+/* estimate_surface (surface.hpp:37-38; surface.cpp:24-62) */
+int pcr_estimate_surface_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene, const double* x,
+                               const uint32_t* ie, uint64_t n, double* p_bar, double* n_bar, double* sdf,
+                               double* weight_sum);
+/* march_segment (surface.hpp:43-47; surface.cpp:64-134); hit = 0 for std::nullopt */
+int pcr_march_segment_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene, const double* origin,
+                            const double* direction, const uint32_t* ie, const double* t_max, uint64_t n,
+                            uint8_t* hit, double* position, double* normal, uint32_t* label, double* distance);
+/* project_to_surface (surface.hpp:50-51; surface.cpp:136-162) */
+int pcr_project_to_surface_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene, const double* x,
+                                 const uint32_t* ie, uint64_t n, uint8_t* hit, double* position, double* normal,
+                                 uint32_t* label);
+/* reception_point_of (voxel_grid.hpp:107; voxel_grid.cpp:61-80) for grid IEs */
+int pcr_reception_point_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene, const uint32_t* ie,
+                              uint64_t n, double* point);
+/* local_frame (surface.hpp:55; surface.cpp:164-177) */
+int pcr_local_frame_batch(pcr_ctx* ctx, const double* normal, uint64_t n, double* u, double* v);
+/* cone_intersects_sphere (tracer.hpp:92; tracer.cpp:129-136) */
+int pcr_cone_intersects_sphere_batch(pcr_ctx* ctx, const double* o, const double* d, const double* alpha,
+                                     const double* c, const double* r, uint64_t n, uint8_t* out);
+/* reflect_ray (tracer.hpp:103-104; tracer.cpp:257-267); ok = 0 for std::nullopt */
+int pcr_reflect_ray_batch(pcr_ctx* ctx, const pcr_grid* grid, const double* hit_position, const double* hit_normal,
+                          const double* incoming, uint64_t n, const pcr_trace_params* params, uint8_t* ok,
+                          pcr_ray_desc* rays);
+/* diffract_rays (tracer.hpp:113-116; tracer.cpp:269-311) at a point on scene edge
+ * edge_index; *rays is library-owned (pcr_free_rays) */
+int pcr_diffract_rays(pcr_ctx* ctx, const pcr_scene* scene, uint32_t edge_index, const double* point,
+                      const double* incoming, const pcr_trace_params* params, pcr_ray_desc** rays, uint64_t* n_rays);
+void pcr_free_rays(pcr_ray_desc* rays);
+
+/* PathNode (refine.hpp:19-45) flattened: kind 0 reflection {c, u, v, normal, r, s,
+ * label}, kind 1 diffraction {c, w = u, t = r, t_min, t_max, label, edge_index} */
+typedef struct pcr_path_node {
+  int32_t kind;
+  uint32_t label, edge_index, pad;
+  double c[3], u[3], v[3], normal[3];
+  double r, s, t_min, t_max;
+} pcr_path_node;
+/* make_path_state (refine.hpp:69; refine.cpp:134-161) for every candidate row:
+ * nodes[i * stride + q] for q < n_inter[i] */
+int pcr_make_path_state(pcr_ctx* ctx, const pcr_scene* scene, const pcr_paths* candidates, pcr_path_node* nodes);
+/* path_length (refine.hpp:71; refine.cpp:163-165) and, when gradients != NULL,
+ * local_gradients (refine.hpp:75; refine.cpp:167-187): gradients[i * 2 * stride + ...]
+ * in the reference's order, gradients_ok[i] = 0 for std::nullopt */
+int pcr_path_eval_batch(pcr_ctx* ctx, const double* tx, const double* rx, const uint32_t* n_nodes,
+                        const pcr_path_node* nodes, uint32_t stride, uint64_t n, double* length, double* gradients,
+                        uint8_t* gradients_ok);
 
 /* ---- stage 3: refinement ---------------------------------------------------- */
 /* refine_path (refine.hpp:77-78; refine.cpp:189-286) over a candidate list */

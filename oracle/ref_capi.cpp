@@ -440,10 +440,11 @@ int pcrref_cone_trace_batch(const void* grid, const void* scene, const pcr_ray_d
       recs[i] = voxel_cone_trace(ray_from_desc(rays[i]), g, s, TraceParams{},
                                  want_debug ? &dbg[i] : nullptr);
     });
-    std::size_t total = 0, total_ev = 0;
+    std::size_t total = 0, total_ev = 0, total_vi = 0;
     for (std::size_t i = 0; i < n_rays; ++i) {
       total += recs[i].size();
       total_ev += dbg[i].evaluated.size();
+      total_vi += dbg[i].visited.size();
     }
     pcr_receptions* r = alloc<pcr_receptions>(1);
     r->n_rays = n_rays;
@@ -458,10 +459,14 @@ int pcrref_cone_trace_batch(const void* grid, const void* scene, const pcr_ray_d
     r->hit_distance = alloc<double>(total);
     r->evaluated_offset = alloc<std::uint64_t>(n_rays + 1);
     r->evaluated = alloc<std::uint32_t>(total_ev);
-    std::size_t k = 0, ke = 0;
+    r->visited_offset = alloc<std::uint64_t>(n_rays + 1);
+    r->visited = alloc<std::uint32_t>(total_vi);
+    std::size_t k = 0, ke = 0, kv = 0;
     for (std::size_t i = 0; i < n_rays; ++i) {
       r->ray_offset[i] = k;
       r->evaluated_offset[i] = ke;
+      r->visited_offset[i] = kv;
+      for (std::uint32_t c : dbg[i].visited) r->visited[kv++] = c;
       for (const Reception& rc : recs[i]) {
         r->ie_index[k] = rc.ie_index;
         put3(r->reception_point + 3 * k, rc.reception_point);
@@ -476,6 +481,7 @@ int pcrref_cone_trace_batch(const void* grid, const void* scene, const pcr_ray_d
     }
     r->ray_offset[n_rays] = k;
     r->evaluated_offset[n_rays] = ke;
+    r->visited_offset[n_rays] = kv;
     *out = r;
   });
 }
@@ -484,7 +490,7 @@ void pcrref_free_receptions(pcr_receptions* r) {
   if (!r) return;
   void* arrays[] = {r->ray_offset, r->ie_index,   r->reception_point, r->hit_valid,
                     r->hit_position, r->hit_normal, r->hit_label,     r->hit_distance,
-                    r->evaluated_offset, r->evaluated};
+                    r->evaluated_offset, r->evaluated, r->visited_offset, r->visited};
   for (void* a : arrays) std::free(a);
   std::free(r);
 }

@@ -155,11 +155,19 @@ class RayDesc(C.Structure):
     ]
 
 
+class PathNode(C.Structure):
+    """pcr_path_node: PathNode (refine.hpp:19-45) flattened."""
+    _fields_ = [("kind", C.c_int32), ("label", C.c_uint32), ("edge_index", C.c_uint32), ("pad", C.c_uint32),
+                ("c", C.c_double * 3), ("u", C.c_double * 3), ("v", C.c_double * 3), ("normal", C.c_double * 3),
+                ("r", C.c_double), ("s", C.c_double), ("t_min", C.c_double), ("t_max", C.c_double)]
+
+
 class Receptions(C.Structure):
     _fields_ = [
         ("n_rays", C.c_uint64), ("n", C.c_uint64), ("ray_offset", _pu64), ("ie_index", _pu32),
         ("reception_point", _pd), ("hit_valid", _pu8), ("hit_position", _pd), ("hit_normal", _pd),
         ("hit_label", _pu32), ("hit_distance", _pd), ("evaluated_offset", _pu64), ("evaluated", _pu32),
+        ("visited_offset", _pu64), ("visited", _pu32),
     ]
 
 
@@ -353,6 +361,7 @@ def receptions_to_dict(r: Receptions) -> dict:
     n, nr = int(r.n), int(r.n_rays)
     off = _arr(r.ray_offset, nr + 1, np.uint64)
     eoff = _arr(r.evaluated_offset, nr + 1, np.uint64)
+    voff = _arr(r.visited_offset, nr + 1, np.uint64)
     return {
         "n_rays": nr, "n": n, "ray_offset": off,
         "ie_index": _arr(r.ie_index, n, np.uint32),
@@ -364,6 +373,8 @@ def receptions_to_dict(r: Receptions) -> dict:
         "hit_distance": _arr(r.hit_distance, n, np.float64),
         "evaluated_offset": eoff,
         "evaluated": _arr(r.evaluated, int(eoff[-1]) if nr else 0, np.uint32),
+        "visited_offset": voff,
+        "visited": _arr(r.visited, int(voff[-1]) if nr else 0, np.uint32),
     }
 
 

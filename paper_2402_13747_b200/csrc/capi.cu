@@ -284,7 +284,8 @@ void pcr_free_summary(pcr_summary* s) {
 void pcr_free_receptions(pcr_receptions* r) {
   if (!r) return;
   void* a[] = {r->ray_offset, r->ie_index,   r->reception_point,  r->hit_valid, r->hit_position,
-               r->hit_normal, r->hit_label,  r->hit_distance,     r->evaluated_offset, r->evaluated};
+               r->hit_normal, r->hit_label,  r->hit_distance,     r->evaluated_offset, r->evaluated,
+               r->visited_offset, r->visited};
   for (void* x : a) std::free(x);
   std::free(r);
 }

@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 
+#include <cctype>
 #include <cerrno>
 #include <cstdio>
 #include <cstdlib>
@@ -25,6 +26,9 @@
 #include <string>
 #include <vector>
 
+#include <algorithm>
+
+#include "exact.cuh"
 #include "host_alloc.hpp"
 #include "pipeline.hpp"
 
@@ -32,19 +36,23 @@ namespace pcr {
 
 namespace {
 
-[[noreturn]] void header_error(int line_no, const std::string& what) {
-  throw Error(PCR_ERR_RUNTIME, "parse error at line " + std::to_string(line_no) + ": " + what);
-}
+// ---- PLY header -------------------------------------------------------------------
+// A PLY header (Turk's format): the magic line "ply", one format line, then
+// `keyword args...` lines up to "end_header". Only the vertex element is read; its
+// scalar properties give the byte layout of a binary row (or the value order of an
+// ascii row). Errors carry the texts and 1-based line numbers load_point_cloud
+// reports (io.cpp:40-122), since callers and tests match them.
 
-size_t ply_type_size(const std::string& type, int line_no) {
-  if (type == "char" || type == "int8" || type == "uchar" || type == "uint8") return 1;
-  if (type == "short" || type == "int16" || type == "ushort" || type == "uint16") return 2;
-  if (type == "int" || type == "int32" || type == "uint" || type == "uint32" || type == "float" ||
-      type == "float32")
-    return 4;
-  if (type == "double" || type == "float64") return 8;
-  header_error(line_no, "unknown property type '" + type + "'");
-}
+// byte sizes of the PLY scalar types, by every name the format allows
+struct PlyType {
+  const char* name;
+  uint32_t bytes;
+};
+constexpr PlyType kPlyTypes[] = {
+    {"char", 1},  {"int8", 1},   {"uchar", 1},  {"uint8", 1},   {"short", 2},   {"int16", 2},
+    {"ushort", 2}, {"uint16", 2}, {"int", 4},    {"int32", 4},   {"uint", 4},    {"uint32", 4},
+    {"float", 4}, {"float32", 4}, {"double", 8}, {"float64", 8},
+};
 
 struct PlyProp {
   std::string type, name;
@@ -58,76 +66,122 @@ struct PlyHeader {
   int idx[7];  // x y z nx ny nz label
 };
 
-// Header rules of load_point_cloud (io.cpp:40-122), same messages.
-PlyHeader parse_header(std::istream& in) {
-  PlyHeader h;
-  int line_no = 0;
-  auto next_line = [&](std::string& line) {
-    if (!std::getline(in, line)) header_error(line_no + 1, "unexpected end of header");
-    ++line_no;
-    if (!line.empty() && line.back() == '\r') line.pop_back();
-  };
-  std::string line;
-  next_line(line);
-  if (line != "ply") header_error(line_no, "expected 'ply' magic");
-  next_line(line);
-  if (line == "format ascii 1.0")
-    h.binary = false;
-  else if (line == "format binary_little_endian 1.0")
-    h.binary = true;
-  else
-    header_error(line_no, "unsupported format '" + line + "'");
-  bool in_vertex = false, vertex_seen = false;
-  for (;;) {
-    next_line(line);
-    std::istringstream iss(line);
-    std::string word;
-    iss >> word;
-    if (word == "comment" || word == "obj_info" || word.empty()) continue;
-    if (word == "end_header") break;
-    if (word == "element") {
-      std::string name;
-      long long count = -1;
-      if (!(iss >> name >> count) || count < 0) header_error(line_no, "malformed element declaration");
-      if (name == "vertex") {
-        if (vertex_seen) header_error(line_no, "duplicate vertex element");
-        vertex_seen = true;
-        in_vertex = true;
-        h.vertex_count = static_cast<size_t>(count);
-      } else {
-        if (!vertex_seen && count > 0) header_error(line_no, "element '" + name + "' precedes vertex data");
-        in_vertex = false;
-      }
-      continue;
-    }
-    if (word == "property") {
-      if (!in_vertex) continue;
-      PlyProp p;
-      iss >> p.type;
-      if (p.type == "list") header_error(line_no, "list property in vertex element");
-      iss >> p.name;
-      if (p.name.empty()) header_error(line_no, "malformed property declaration");
-      p.offset = h.stride;
-      h.stride += ply_type_size(p.type, line_no);
-      h.props.push_back(p);
-      continue;
-    }
-    header_error(line_no, "unknown header keyword '" + word + "'");
+// whitespace-separated words of a header line
+std::vector<std::string> split_words(const std::string& line) {
+  std::vector<std::string> w;
+  size_t i = 0;
+  while (i < line.size()) {
+    while (i < line.size() && std::isspace(static_cast<unsigned char>(line[i]))) ++i;
+    const size_t b = i;
+    while (i < line.size() && !std::isspace(static_cast<unsigned char>(line[i]))) ++i;
+    if (i > b) w.emplace_back(line, b, i - b);
   }
-  if (!vertex_seen) header_error(line_no, "no vertex element");
-  const char* required[] = {"x", "y", "z", "nx", "ny", "nz", "label"};
-  for (int r = 0; r < 7; ++r) {
-    h.idx[r] = -1;
-    for (size_t i = 0; i < h.props.size(); ++i)
-      if (h.props[i].name == required[r]) h.idx[r] = static_cast<int>(i);  // last declaration wins
-    if (h.idx[r] < 0) throw Error(PCR_ERR_RUNTIME, std::string("missing field: ") + required[r]);
-    const std::string& t = h.props[h.idx[r]].type;
-    if (r < 6 && t != "float" && t != "float32")
-      throw Error(PCR_ERR_RUNTIME, std::string("field ") + required[r] + " must be float32");
-    if (r == 6 && t != "uint" && t != "uint32") throw Error(PCR_ERR_RUNTIME, "field label must be uint32");
-  }
-  return h;
+  return w;
 }
+
+// decimal integer at the start of `word` (optional sign, then digits; trailing
+// characters ignored, as a formatted stream read stops there); false if none or out
+// of range
+bool leading_integer(const std::string& word, long long& v) {
+  errno = 0;
+  char* end = nullptr;
+  const char* b = word.c_str();
+  if (*b != '+' && *b != '-' && !std::isdigit(static_cast<unsigned char>(*b))) return false;
+  v = std::strtoll(b, &end, 10);
+  return end != b && errno != ERANGE;
+}
+
+class PlyHeaderReader {
+ public:
+  explicit PlyHeaderReader(std::istream& in) : in_(in) {}
+
+  PlyHeader read() {
+    if (line() != "ply") fail("expected 'ply' magic");
+    const std::string& fmt = line();
+    if (fmt == "format ascii 1.0")
+      h_.binary = false;
+    else if (fmt == "format binary_little_endian 1.0")
+      h_.binary = true;
+    else
+      fail("unsupported format '" + fmt + "'");
+    for (;;) {
+      const std::vector<std::string> w = split_words(line());
+      if (w.empty() || w[0] == "comment" || w[0] == "obj_info") continue;
+      if (w[0] == "end_header") break;
+      if (w[0] == "element")
+        element(w);
+      else if (w[0] == "property")
+        property(w);
+      else
+        fail("unknown header keyword '" + w[0] + "'");
+    }
+    if (!vertex_seen_) fail("no vertex element");
+    static const char* const kRequired[7] = {"x", "y", "z", "nx", "ny", "nz", "label"};
+    for (int r = 0; r < 7; ++r) {
+      int found = -1;  // a repeated name: the last declaration is the one read
+      for (int i = static_cast<int>(h_.props.size()) - 1; i >= 0 && found < 0; --i)
+        if (h_.props[i].name == kRequired[r]) found = i;
+      if (found < 0) throw Error(PCR_ERR_RUNTIME, std::string("missing field: ") + kRequired[r]);
+      const std::string& t = h_.props[found].type;
+      const bool is_f32 = t == "float" || t == "float32", is_u32 = t == "uint" || t == "uint32";
+      if (r < 6 && !is_f32) throw Error(PCR_ERR_RUNTIME, std::string("field ") + kRequired[r] + " must be float32");
+      if (r == 6 && !is_u32) throw Error(PCR_ERR_RUNTIME, "field label must be uint32");
+      h_.idx[r] = found;
+    }
+    return h_;
+  }
+
+ private:
+  // "element <name> <count>": only the vertex element is kept; any element with rows
+  // declared before it would have to be skipped in the body, which is not supported
+  void element(const std::vector<std::string>& w) {
+    long long count = -1;
+    if (w.size() < 3 || !leading_integer(w[2], count) || count < 0) fail("malformed element declaration");
+    in_vertex_ = w[1] == "vertex";
+    if (in_vertex_) {
+      if (vertex_seen_) fail("duplicate vertex element");
+      vertex_seen_ = true;
+      h_.vertex_count = static_cast<size_t>(count);
+    } else if (!vertex_seen_ && count > 0) {
+      fail("element '" + w[1] + "' precedes vertex data");
+    }
+  }
+  // "property <type> <name>" inside the vertex element: appended to the row layout
+  void property(const std::vector<std::string>& w) {
+    if (!in_vertex_) return;
+    const std::string type = w.size() > 1 ? w[1] : std::string();
+    if (type == "list") fail("list property in vertex element");
+    if (w.size() < 3) fail("malformed property declaration");
+    uint32_t bytes = 0;
+    for (const PlyType& t : kPlyTypes)
+      if (type == t.name) bytes = t.bytes;
+    if (!bytes) fail("unknown property type '" + type + "'");
+    h_.props.push_back(PlyProp{type, w[2], h_.stride});
+    h_.stride += bytes;
+  }
+  // the next header line (CR of a CRLF file dropped); running out is an error on the
+  // line after the last one read
+  const std::string& line() {
+    if (!std::getline(in_, cur_)) {
+      ++n_;
+      fail("unexpected end of header");
+    }
+    ++n_;
+    if (!cur_.empty() && cur_.back() == '\r') cur_.pop_back();
+    return cur_;
+  }
+  [[noreturn]] void fail(const std::string& what) const {
+    throw Error(PCR_ERR_RUNTIME, "parse error at line " + std::to_string(n_) + ": " + what);
+  }
+
+  std::istream& in_;
+  std::string cur_;
+  int n_ = 0;
+  bool in_vertex_ = false, vertex_seen_ = false;
+  PlyHeader h_;
+};
+
+PlyHeader parse_header(std::istream& in) { return PlyHeaderReader(in).read(); }
 
 struct RowLayout {
   uint32_t stride;
@@ -316,56 +370,56 @@ void api_write_paths(const char* path, const pcr_paths& p, uint64_t config_hash)
 
 namespace {
 
-double sq3(const double* v) { return (v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]; }
+// One line of an edges file: `start(3) end(3) normal_a(3) normal_b(3) label`, anything
+// after '#' ignored. Numbers are read as formatted stream extraction reads a double
+// (the reference's grammar and rounding), left to right.
+enum class EdgeLine { kSkip, kShort, kRecord };
+
+EdgeLine read_edge_line(std::string text, double v[13]) {
+  text.resize(std::min(text.size(), text.find('#')));
+  std::istringstream fields(text);
+  int got = 0;
+  while (got < 13 && fields >> v[got]) ++got;
+  // a line whose first field is not a number carries no record (blank, comment, prose)
+  return got == 0 ? EdgeLine::kSkip : got < 13 ? EdgeLine::kShort : EdgeLine::kRecord;
+}
+
+// The record's geometry checks (DiffractionEdge invariants, io.cpp:209-222): a
+// non-degenerate segment, non-zero normals, and after normalisation both normals
+// perpendicular to the edge direction within 1e-3. Normalises v[6..11] in place;
+// returns the defect or nullptr.
+const char* edge_defect(double v[13]) {
+  const V3 a{v[0], v[1], v[2]}, b{v[3], v[4], v[5]};
+  V3 na{v[6], v[7], v[8]}, nb{v[9], v[10], v[11]};
+  if (norm(b - a) < 1e-12) return "degenerate edge";
+  if (norm(na) < 1e-12 || norm(nb) < 1e-12) return "zero normal";
+  na = normalized(na);
+  nb = normalized(nb);
+  const V3 w = normalized(b - a);
+  if (std::abs(dot(w, na)) > 1e-3 || std::abs(dot(w, nb)) > 1e-3) return "normal not perpendicular to edge";
+  const double n6[6] = {na.x, na.y, na.z, nb.x, nb.y, nb.z};
+  std::copy(n6, n6 + 6, v + 6);
+  return nullptr;
+}
 
 }  // namespace
 
-// load_edges (io.cpp:191-229): records are parsed with istream >> double like the
-// reference (same grammar, same rounding, same failure points); per record the edge
-// must be non-degenerate (|end - start| >= 1e-12), both normals non-zero, and after
-// normalisation (v / sqrt(v.v), Eigen's normalize) perpendicular to the edge direction
-// within 1e-3.
+// load_edges (io.cpp:191-229): geometry rows (start, end, unit normal_a, unit
+// normal_b) and labels; the n-th accepted record is "edge record n" in errors.
 void api_load_edges(const char* path, std::vector<double>& geom, std::vector<uint32_t>& label) {
   std::ifstream in(path);
   if (!in) throw Error(PCR_ERR_RUNTIME, std::string("cannot open edges file: ") + path);
   geom.clear();
   label.clear();
-  std::string line;
-  size_t record = 0;
-  auto fail = [&](const char* what) {
-    throw Error(PCR_ERR_RUNTIME, "edge record " + std::to_string(record) + ": " + what);
-  };
-  while (std::getline(in, line)) {
-    const size_t hash = line.find('#');
-    if (hash != std::string::npos) line.erase(hash);
-    std::istringstream iss(line);
+  std::string text;
+  while (std::getline(in, text)) {
     double v[13];
-    if (!(iss >> v[0])) continue;  // blank or comment-only line
-    for (int i = 1; i < 13; ++i)
-      if (!(iss >> v[i])) fail("expected 13 values");
-    double d[3] = {v[3] - v[0], v[4] - v[1], v[5] - v[2]};
-    if (std::sqrt(sq3(d)) < 1e-12) fail("degenerate edge");
-    double* na = v + 6;
-    double* nb = v + 9;
-    if (std::sqrt(sq3(na)) < 1e-12 || std::sqrt(sq3(nb)) < 1e-12) fail("zero normal");
-    for (double* n : {na, nb}) {
-      const double z = sq3(n);
-      if (z > 0) {
-        const double r = std::sqrt(z);
-        for (int a = 0; a < 3; ++a) n[a] /= r;
-      }
-    }
-    const double dz = sq3(d);
-    if (dz > 0) {
-      const double r = std::sqrt(dz);
-      for (int a = 0; a < 3; ++a) d[a] /= r;
-    }
-    const double wa = (d[0] * na[0] + d[1] * na[1]) + d[2] * na[2];
-    const double wb = (d[0] * nb[0] + d[1] * nb[1]) + d[2] * nb[2];
-    if (std::abs(wa) > 1e-3 || std::abs(wb) > 1e-3) fail("normal not perpendicular to edge");
+    const EdgeLine kind = read_edge_line(text, v);
+    if (kind == EdgeLine::kSkip) continue;
+    const char* defect = kind == EdgeLine::kShort ? "expected 13 values" : edge_defect(v);
+    if (defect) throw Error(PCR_ERR_RUNTIME, "edge record " + std::to_string(label.size()) + ": " + defect);
     geom.insert(geom.end(), v, v + 12);
     label.push_back(static_cast<uint32_t>(v[12]));
-    ++record;
   }
 }
 

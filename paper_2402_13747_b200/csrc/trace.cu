@@ -36,34 +36,11 @@ struct TraceCfg {
   double apex;
 };
 
-struct FanTable {
-  const double* t;  // n*6
-  int n;
-};
-
 namespace {
 
 constexpr int kT = 256;
 
 __device__ __forceinline__ uint32_t atomic_append(uint32_t* counter) { return atomicAdd(counter, 1u); }
-
-// diffract_rays degeneracy tests (tracer.cpp:275-284); returns false for "no rays".
-__device__ __forceinline__ bool fan_frame(const double* edge, const V3& incoming, V3& w, V3& e1, V3& e2,
-                                          double& cos_b, double& sin_b, V3& na, V3& nb) {
-  const V3 s = load3(edge), e = load3(edge + 3);
-  na = load3(edge + 6);
-  nb = load3(edge + 9);
-  w = normalized(e - s);
-  cos_b = dot(incoming, w);
-  if (fabs(cos_b) > 0.999) return false;
-  if (libm_le(angle_between(na, nb), 1e-9, 4.0)) return false;  // atan2: see libm_le
-  if (dot(incoming, na) >= 0.0 && dot(incoming, nb) >= 0.0) return false;
-  e1 = safe_normalized(incoming - cos_b * w);
-  if (is_zero(e1)) return false;
-  e2 = cross(w, e1);
-  sin_b = sqrt(smax(0.0, 1.0 - cos_b * cos_b));
-  return true;
-}
 
 // Builds ray j of a node's children. Reflection: j == 0. Returns alive.
 __device__ __forceinline__ bool make_ray(const Node& nd, uint32_t node_idx, uint32_t j, const GridView& g,
@@ -630,6 +607,33 @@ __global__ void evaluated_kernel(const Ray* __restrict__ rays, uint32_t n, GridV
   if (count) count[k] = c;
 }
 
+// TraceDebug::visited (tracer.cpp:333-335, 391-397): the walker's voxels, jumps
+// over empty space (march >= 2) included, in walk order
+__global__ void visited_kernel(const Ray* __restrict__ rays, uint32_t n, GridView g,
+                               const uint64_t* __restrict__ offset, uint32_t* __restrict__ count,
+                               uint32_t* __restrict__ out) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  uint32_t c = 0;
+  if (g.n_ies) {
+    const Ray r = rays[k];
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+    Walker w;
+    w.init(g, r.o, r.d, 0.0, inf);
+    while (w.active) {
+      const uint32_t vi = linear_index(g, w.v[0], w.v[1], w.v[2]);
+      if (out) out[offset[k] + c] = vi;
+      ++c;
+      const int march = g.cells[vi].z;
+      if (march >= 2)
+        w.init(g, r.o, r.d, w.t_entry + static_cast<double>(march - 1) * g.voxel_size, inf);
+      else
+        w.advance(g);
+    }
+  }
+  if (count) count[k] = c;
+}
+
 struct RecOut {
   uint8_t* ok;
   uint8_t* hit_valid;
@@ -691,7 +695,7 @@ unsigned nb(uint64_t n, unsigned t = kT) { return static_cast<unsigned>((n + t -
 // ========================================================================================
 // host side
 
-static void ensure_fan_table(Ctx& ctx, int n) {
+void ensure_fan(Ctx& ctx, int n) {
   if (ctx.fan_n == n && ctx.fan_table.get()) return;
   // diffract_rays (tracer.cpp:288-301): phi = j * dphi, dphi = 2 pi / n; the sines and
   // cosines depend on (j, n) only and are evaluated once here with the host libm.
@@ -904,7 +908,7 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
   const uint32_t n_local = n_hits > shard ? (n_hits - shard + n_shards - 1) / n_shards : 0;
   if (p.max_interactions < 1 || n_local == 0) return;
   if (p.max_interactions > kMaxDepth) throw Error(1, "trace: max_interactions above the supported 8");
-  if (p.max_diffractions >= 1 || true) ensure_fan_table(ctx, std::max(1, c.fan_n));
+  if (p.max_diffractions >= 1 || true) ensure_fan(ctx, std::max(1, c.fan_n));
   const FanTable fan{ctx.fan_table.get(), c.fan_n};
   const GridView gv = grid.view();
   const SceneView sv = scene.view();
@@ -1497,6 +1501,29 @@ void api_cone_trace_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, 
     ev.resize(eoff[n_rays]);
     d2h(ev.data(), dev.get(), ev.size(), s);
   }
+  // visited voxels (TraceDebug)
+  std::vector<uint64_t> voff(n_rays + 1, 0);
+  std::vector<uint32_t> vv;
+  if (want_debug && n_rays) {
+    DBuf<uint32_t> vcnt(m, s);
+    count_launch();
+    visited_kernel<<<nb(n_rays, 128), 128, 0, s>>>(rays.get(), static_cast<uint32_t>(n_rays), gv, nullptr,
+                                                   vcnt.get(), nullptr);
+    PCR_LAUNCH_CHECK();
+    std::vector<uint32_t> hc(n_rays);
+    d2h(hc.data(), vcnt.get(), n_rays, s);
+    PCR_CUDA(cudaStreamSynchronize(s));
+    for (size_t k = 0; k < n_rays; ++k) voff[k + 1] = voff[k] + hc[k];
+    DBuf<uint64_t> doff(n_rays + 1, s);
+    h2d(doff.get(), voff.data(), n_rays + 1, s);
+    DBuf<uint32_t> dvv(voff[n_rays] ? voff[n_rays] : 1, s);
+    count_launch();
+    visited_kernel<<<nb(n_rays, 128), 128, 0, s>>>(rays.get(), static_cast<uint32_t>(n_rays), gv, doff.get(),
+                                                   nullptr, dvv.get());
+    PCR_LAUNCH_CHECK();
+    vv.resize(voff[n_rays]);
+    d2h(vv.data(), dvv.get(), vv.size(), s);
+  }
   PCR_CUDA(cudaStreamSynchronize(s));
   // group by ray, ascending ie (tracer.cpp:400-401)
   std::vector<uint32_t> order;
@@ -1520,6 +1547,8 @@ void api_cone_trace_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, 
   r->hit_distance = halloc<double>(nrec);
   r->evaluated_offset = halloc<uint64_t>(n_rays + 1);
   r->evaluated = halloc<uint32_t>(ev.size());
+  r->visited_offset = halloc<uint64_t>(n_rays + 1);
+  r->visited = halloc<uint32_t>(vv.size());
   size_t k = 0;
   for (uint64_t ray = 0; ray < n_rays; ++ray) {
     r->ray_offset[ray] = k;
@@ -1545,6 +1574,8 @@ void api_cone_trace_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, 
   r->ray_offset[n_rays] = k;
   for (uint64_t ray = 0; ray <= n_rays; ++ray) r->evaluated_offset[ray] = eoff[ray];
   if (!ev.empty()) std::memcpy(r->evaluated, ev.data(), ev.size() * sizeof(uint32_t));
+  for (uint64_t ray = 0; ray <= n_rays; ++ray) r->visited_offset[ray] = voff[ray];
+  if (!vv.empty()) std::memcpy(r->visited, vv.data(), vv.size() * sizeof(uint32_t));
   *out = r;
 }
 

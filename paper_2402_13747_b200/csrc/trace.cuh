@@ -323,4 +323,30 @@ __device__ __forceinline__ void warp_add_u64(unsigned long long* dst, unsigned l
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
 }
 
+// Keller-fan sin/cos table (host libm, trace.cu ensure_fan): per j cos phi, sin phi,
+// sin/cos(phi + dphi/2), sin/cos(phi - dphi/2)
+struct FanTable {
+  const double* t;  // n*6
+  int n;
+};
+
+// diffract_rays degeneracy tests (tracer.cpp:275-284); returns false for "no rays".
+__device__ __forceinline__ bool fan_frame(const double* edge, const V3& incoming, V3& w, V3& e1, V3& e2,
+                                          double& cos_b, double& sin_b, V3& na, V3& nb) {
+  const V3 s = load3(edge), e = load3(edge + 3);
+  na = load3(edge + 6);
+  nb = load3(edge + 9);
+  w = normalized(e - s);
+  cos_b = dot(incoming, w);
+  if (fabs(cos_b) > 0.999) return false;
+  if (libm_le(angle_between(na, nb), 1e-9, 4.0)) return false;  // atan2: see libm_le
+  if (dot(incoming, na) >= 0.0 && dot(incoming, nb) >= 0.0) return false;
+  e1 = safe_normalized(incoming - cos_b * w);
+  if (is_zero(e1)) return false;
+  e2 = cross(w, e1);
+  sin_b = sqrt(smax(0.0, 1.0 - cos_b * cos_b));
+  return true;
+}
+
+
 }  // namespace pcr

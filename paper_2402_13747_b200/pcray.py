@@ -57,6 +57,21 @@ def lib():
         L.pcr_propagate.argtypes = [vp, vp, vp, C.c_uint32, pp(abi.InitialHits), pp(abi.TraceParams),
                                     pp(pp(abi.Paths))]
         L.pcr_last_trace_stats.argtypes = [vp, pp(C.c_uint64)]
+        pd, pu32, pu8 = pp(C.c_double), pp(C.c_uint32), pp(C.c_uint8)
+        L.pcr_estimate_surface_batch.argtypes = [vp, vp, vp, pd, pu32, C.c_uint64, pd, pd, pd, pd]
+        L.pcr_march_segment_batch.argtypes = [vp, vp, vp, pd, pd, pu32, pd, C.c_uint64, pu8, pd, pd, pu32, pd]
+        L.pcr_project_to_surface_batch.argtypes = [vp, vp, vp, pd, pu32, C.c_uint64, pu8, pd, pd, pu32]
+        L.pcr_local_frame_batch.argtypes = [vp, pd, C.c_uint64, pd, pd]
+        L.pcr_reception_point_batch.argtypes = [vp, vp, vp, pu32, C.c_uint64, pd]
+        L.pcr_cone_intersects_sphere_batch.argtypes = [vp, pd, pd, pd, pd, pd, C.c_uint64, pu8]
+        L.pcr_reflect_ray_batch.argtypes = [vp, vp, pd, pd, pd, C.c_uint64, pp(abi.TraceParams), pu8,
+                                            pp(abi.RayDesc)]
+        L.pcr_diffract_rays.argtypes = [vp, vp, C.c_uint32, pd, pd, pp(abi.TraceParams), pp(pp(abi.RayDesc)),
+                                        pp(C.c_uint64)]
+        L.pcr_free_rays.argtypes = [pp(abi.RayDesc)]
+        L.pcr_free_rays.restype = None
+        L.pcr_make_path_state.argtypes = [vp, vp, pp(abi.Paths), pp(abi.PathNode)]
+        L.pcr_path_eval_batch.argtypes = [vp, pd, pd, pu32, pp(abi.PathNode), C.c_uint32, C.c_uint64, pd, pd, pu8]
         L.pcr_cone_trace_batch.argtypes = [vp, vp, vp, pp(abi.RayDesc), C.c_uint64, C.c_int,
                                            pp(pp(abi.Receptions))]
         L.pcr_segment_visible_batch.argtypes = [vp, vp, vp, pp(C.c_double), pp(C.c_double), pp(C.c_uint32),
@@ -107,7 +122,10 @@ EXPORTED_SYMBOLS = [
     "pcr_free_summary", "pcr_free_receptions", "pcr_run_pipeline_device", "pcr_shard_trace", "pcr_shard_rows",
     "pcr_shard_refine", "pcr_shard_outcomes", "pcr_shard_stats_get", "pcr_shard_finish", "pcr_scene_load_ply",
     "pcr_scene_points", "pcr_write_paths", "pcr_libm_exp_batch", "pcr_load_edges", "pcr_free_edges",
-    "pcr_run_pipeline", "pcr_last_trace_stats",
+    "pcr_run_pipeline", "pcr_last_trace_stats", "pcr_estimate_surface_batch", "pcr_march_segment_batch",
+    "pcr_project_to_surface_batch", "pcr_local_frame_batch", "pcr_cone_intersects_sphere_batch",
+    "pcr_reflect_ray_batch", "pcr_diffract_rays", "pcr_free_rays", "pcr_make_path_state", "pcr_path_eval_batch",
+    "pcr_reception_point_batch",
 ]
 
 

@@ -143,6 +143,9 @@ def test_voxel_cone_trace_batch(oracle, built, name):
         b = ref["evaluated"][ref["evaluated_offset"][k]:ref["evaluated_offset"][k + 1]]
         assert len(a) == len(set(a.tolist()))
         assert sorted(a.tolist()) == sorted(b.tolist()), f"ray {k}"
+    # TraceDebug.visited: the walker's voxels in walk order (jumps included), exactly
+    assert_bitwise("visited_offset", got["visited_offset"], ref["visited_offset"])
+    assert_bitwise("visited", got["visited"], ref["visited"])
 
 
 @pytest.mark.parametrize("name,mi,md", [("box_room", 1, 0), ("box_room", 2, 0), ("screen_edge", 2, 1),
