@@ -51,6 +51,9 @@ struct GridView {
   const uint32_t* nb_lab = nullptr;  // label of each list entry (lists are stably sorted by label)
   const double4* nb_pa = nullptr;    // per entry: plane point, sphere radius
   const double4* nb_pb = nullptr;    // per entry: plane normal
+  // exact fast rejection in the planar reprojection scan (refine.cu planar_candidate_at):
+  // set when the scene's coordinates are small enough for its error bound
+  int fast_reject = 0;
 };
 
 // Device-resident Scene (scene.hpp:38-46).

@@ -79,9 +79,20 @@ __device__ __forceinline__ int voxel_floor(double p, double o, double vs) {
 // (same normal and plane-offset bits, e.g. the IEs of one wall) share t*: the
 // division is done once per plane (cache c_num, c_dn -> c_t). Returns true and
 // lowers best_t when this IE's hit is strictly nearer.
+//
+// Fast rejection (exact): the sdf along the ray is f(t) = dot((o + t d) - pp, n), and
+// in exact arithmetic f(t) = dn (t - t_e) with t_e the plane crossing. The computed
+// f(t) and the computed dn (t - t*) differ by at most ~30 u (|o| + |pp| + |t|)
+// (u = 2^-53: the dot products' rounding, num and dn's rounding, the division), which
+// kMarginFast bounds whenever the scene's coordinates are below ~10^5 m (refine_device
+// sets fast_reject from the grid's extent). So when t* lies outside the window by more
+// than (eps + kMarginFast) / |dn|, both endpoint values have |f| > eps and the same
+// sign: the reference's march returns no hit, decided without evaluating them.
+constexpr double kMarginFast = 1e-9;
 __device__ __forceinline__ bool planar_candidate_at(const V3& prev, const V3& dir, const V3& pp, const V3& pn,
                                                     double eps, double t_lo, double t_hi, double& best_t,
-                                                    long long& c_num, long long& c_dn, double& c_t) {
+                                                    long long& c_num, long long& c_dn, double& c_t,
+                                                    bool fast = false) {
   if (t_hi <= t_lo) return false;
   const double dn = dot(dir, pn);
   const bool snap = fabs(dn) > 1e-12;
@@ -98,6 +109,10 @@ __device__ __forceinline__ bool planar_candidate_at(const V3& prev, const V3& di
   }
   const bool in_win = snap && t_star >= t_lo && t_star <= t_hi;
   if (in_win && t_star >= best_t) return false;
+  if (fast && snap && !in_win) {
+    const double gap = t_star < t_lo ? t_lo - t_star : t_star - t_hi;
+    if (fabs(dn) * gap > eps + kMarginFast) return false;
+  }
   double tc;
   const double f = dot((prev + t_lo * dir) - pp, pn);
   if (fabs(f) <= eps) {
@@ -907,6 +922,12 @@ struct ScanCache {
   uint32_t n_march;
 };
 
+// read-only global loads of a 32-byte record (the scan's arrays never change in a launch)
+__device__ __forceinline__ double4 ldg4(const double4* p) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
 // the warps' scan slots and round owner maps (file scope, so the out-of-line scan
 // addresses them as shared memory rather than through generic pointers)
 __shared__ ScanSlot g_slots[kRefineThreads];
@@ -937,6 +958,7 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
   const double4* __restrict__ nb_pa = g.nb_pa;
   const double4* __restrict__ nb_pb = g.nb_pb;
   const double eps = g.hit_eps;
+  const bool fast = g.fast_reject != 0;
   long long c_num = cache->c_num, c_dn = cache->c_dn;
   double c_t = cache->c_t;
   uint32_t n_march = cache->n_march;
@@ -970,9 +992,9 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
       const ScanSlot& sl = ws[o];
       const uint32_t j = sl.j0 + (F - sl.pre);
       // the record and its plane side by side (no dependent load through the IE index)
-      const double4 r4 = nb_rec[j];
-      const double4 pa = nb_pa[j];
-      const double4 pb = nb_pb[j];
+      const double4 r4 = ldg4(nb_rec + j);
+      const double4 pa = ldg4(nb_pa + j);
+      const double4 pb = ldg4(nb_pb + j);
       const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r4.w));
       const uint32_t ie = static_cast<uint32_t>(w >> 33);
       const V3 sc = ld3(r4);
@@ -986,7 +1008,7 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
         double bt = sl.best_t;
         if (t_lo < bt) {
           if (__builtin_expect(((w >> 32) & 1u) != 0, 1)) {  // planar records are the common case
-            if (planar_candidate_at(pv, dv, ld3(pa), ld3(pb), eps, t_lo, t_center + rad, bt, c_num, c_dn, c_t))
+            if (planar_candidate_at(pv, dv, ld3(pa), ld3(pb), eps, t_lo, t_center + rad, bt, c_num, c_dn, c_t, fast))
               t = bt;
           } else {
             t = march_np(pv.x, pv.y, pv.z, dv.x, dv.y, dv.z, ie, g, s, bt);
@@ -995,6 +1017,12 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
       }
     } else {
       o = 32;  // no record: a segment of its own
+    }
+    carry = __shfl_sync(kFull, o, 31);
+    // rounds without a hit (every record pruned or missed) leave the owners' bests as they are
+    if (!__any_sync(kFull, t < inf)) {
+      __syncwarp();
+      continue;
     }
     // segmented (t, F) min towards each segment's first lane; ties keep the lower F.
     // Segments are the owners' runs within the round: they start at lane 0 and at the
@@ -1012,7 +1040,6 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
         bf = of;
       }
     }
-    carry = __shfl_sync(kFull, o, 31);
     __syncwarp();
     if (valid && ((heads >> lane) & 1u) && bt < ws[o].best_t) {
       ws[o].best_t = bt;
@@ -1278,6 +1305,21 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     gv.ie_rr = rr.get();
     gv.rr_uniform = grid.n_ies && !h;
     gv.rr_radius = r0;
+  }
+  {
+    // planar_candidate_at's fast rejection: prev, pp and the window lie in the grid box
+    // (nodes are reprojected onto IEs inside it; TX/RX are inside scene_bounds), so
+    // |prev| + |pp| + |t| <= 2 R + diam with R the farthest box corner from the origin;
+    // its rounding bound 30 u (2 R + diam) must stay 4x below kMarginFast
+    double r2 = 0.0, d2 = 0.0;
+    for (int a = 0; a < 3; ++a) {
+      const double lo = (&grid.origin.x)[a], hi = lo + grid.dims[a] * grid.voxel_size;
+      const double m = std::fabs(lo) > std::fabs(hi) ? std::fabs(lo) : std::fabs(hi);
+      r2 += m * m;
+      d2 += (hi - lo) * (hi - lo);
+    }
+    const double extent = 2.0 * std::sqrt(r2) + std::sqrt(d2) + 1.0;
+    gv.fast_reject = 4.0 * 30.0 * 1.1102230246251565e-16 * extent < kMarginFast ? 1 : 0;
   }
   // neighbourhood lists (the reprojection box is a cell's 3x3x3 neighbourhood whenever
   // 2 * subvoxel_edge spans exactly one voxel each way, i.e. division_factor 2)
