@@ -272,6 +272,21 @@ int pcr_transmission_phase(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* 
 int pcr_propagate(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene, uint32_t tx_index,
                   const pcr_initial_hits* hits, const pcr_trace_params* params,
                   pcr_paths** out);
+/* ---- sharded voxelization -----------------------------------------------
+ * build_grid split over n_shards processes by contiguous voxel ranges of about
+ * n_points / n_shards points each (each shard holds the whole scene; splitters are
+ * computed identically on every shard). pcr_grid_part_build builds shard `shard`'s
+ * part on the context and returns its size in bytes; pcr_grid_part_copy writes it to a
+ * device buffer; the caller all-gathers the parts (NCCL) and pcr_grid_assemble turns
+ * them, in shard order, into the grid pcr_build_grid would have built, bit for bit
+ * (IE records and point_indices concatenated, point ranges shifted, cells and the
+ * Chebyshev field computed on the assembled grid). */
+int pcr_grid_part_build(pcr_ctx* ctx, const pcr_scene* scene, const pcr_voxel_params* params, uint32_t shard,
+                        uint32_t n_shards, uint64_t* part_bytes);
+int pcr_grid_part_copy(pcr_ctx* ctx, void* dst_device);
+int pcr_grid_assemble(pcr_ctx* ctx, const void* parts_device, const uint64_t* part_offset, const uint64_t* part_bytes,
+                      uint32_t n_parts, pcr_grid** out);
+
 /* work counters of the last pcr_propagate on this context: [0] voxel_cone_trace
  * invocations (= the reference's dfs_trace calls, tracer.cpp:420), [1] visibility
  * tests, [2] cells and [3] IE records the cone walk read (SURVEY 8d units), [4]

@@ -153,6 +153,15 @@ struct Cache {
       }
     return nullptr;
   }
+  H* take(uint64_t key) {  // remove an entry without freeing its handle
+    for (auto it = lru.begin(); it != lru.end(); ++it)
+      if (it->key == key) {
+        H* h = it->h;
+        lru.erase(it);
+        return h;
+      }
+    return nullptr;
+  }
   H* put(uint64_t key, H* h) {
     lru.push_front({key, h});
     while (lru.size() > cap) {
@@ -260,9 +269,16 @@ VoxelGrid grid_from_host(const pcr_grid_host& h) {
   return g;
 }
 
+pcr_grid* upload_grid(const VoxelGrid& g);
+
 pcr_grid* device_grid(const VoxelGrid& g) {
   const uint64_t key = fingerprint(g);
   if (pcr_grid* h = grid_cache().find(key)) return h;
+  return grid_cache().put(key, upload_grid(g));
+}
+
+// a new device copy of a host grid (not cached)
+pcr_grid* upload_grid(const VoxelGrid& g) {
   const size_t nc = g.cells.size(), ni = g.ies.size();
   std::vector<uint32_t> cb(nc), ce(nc), lab(ni), pb(ni), pe(ni), ed(ni), rx(ni), vox(ni), sub(ni);
   std::vector<int32_t> mar(nc);
@@ -323,7 +339,7 @@ pcr_grid* device_grid(const VoxelGrid& g) {
   h.point_indices = pidx.data();
   pcr_grid* d = nullptr;
   check(pcr_grid_upload(ctx(), &h, &d));
-  return grid_cache().put(key, d);
+  return d;
 }
 
 // IE index of `ie` inside `grid` (the helpers take an IE by reference into grid.ies)
@@ -505,16 +521,25 @@ VoxelGrid build_grid(const Scene& scene, const VoxelizationParams& params) {
     check(rc);
   }
   VoxelGrid out = grid_from_host(*h.p);
-  grid_cache().put(fingerprint(out), g);  // later calls on this grid reuse the built handle
+  const uint64_t key = fingerprint(out);
+  if (pcr_grid* old = grid_cache().take(key)) pcr_grid_free(old);  // the same content built again
+  grid_cache().put(key, g);  // later calls on this grid reuse the built handle
   return out;
 }
 
 void compute_march_distances(VoxelGrid& grid) {
   std::lock_guard<std::recursive_mutex> lock(g_mu);
-  pcr_grid* g = device_grid(grid);
-  check(pcr_compute_march_distances(ctx(), g));
+  // the device grid changes with the host one: it leaves the cache under the old
+  // content's key and re-enters under the new one
+  pcr_grid* g = grid_cache().take(fingerprint(grid));
+  if (!g) g = upload_grid(grid);
+  const int rc = pcr_compute_march_distances(ctx(), g);
   Owned<pcr_grid_host> h(pcr_free_grid_host);
-  check(pcr_grid_download(ctx(), g, &h.p));
+  const int rc2 = rc == PCR_OK ? pcr_grid_download(ctx(), g, &h.p) : rc;
+  if (rc2 != PCR_OK) {
+    pcr_grid_free(g);
+    check(rc2);
+  }
   for (size_t c = 0; c < grid.cells.size(); ++c) grid.cells[c].march = h.p->cell_march[c];
   grid_cache().put(fingerprint(grid), g);
 }

@@ -307,6 +307,41 @@ int pcr_propagate(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene* scene, ui
   });
 }
 
+// ---- sharded voxelization (gridparts.cu) -----------------------------------
+int pcr_grid_part_build(pcr_ctx* ctx, const pcr_scene* scene, const pcr_voxel_params* p, uint32_t shard,
+                        uint32_t n_shards, uint64_t* part_bytes) {
+  return guarded(ctx, [&] {
+    if (!scene || !p || !part_bytes) throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    auto part = std::make_unique<pcr::GridDev>();
+    const pcr::VoxelShard vs{shard, n_shards};
+    try {
+      pcr::build_grid_device(ctx->c, scene->s, p->voxel_size, p->division_factor, p->max_cells, *part, &vs);
+    } catch (const pcr::Error& e) {
+      throw pcr::Error(e.code, std::string(e.what()));
+    }
+    *part_bytes = pcr::grid_part_bytes(*part);
+    ctx->c.grid_part = std::move(part);
+  });
+}
+
+int pcr_grid_part_copy(pcr_ctx* ctx, void* dst_device) {
+  return guarded(ctx, [&] {
+    if (!ctx->c.grid_part) throw pcr::Error(PCR_ERR_INVALID, "voxelize: no grid part built on this context");
+    if (!dst_device) throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    pcr::grid_part_serialize(ctx->c, *ctx->c.grid_part, dst_device);
+  });
+}
+
+int pcr_grid_assemble(pcr_ctx* ctx, const void* parts_device, const uint64_t* part_offset, const uint64_t* part_bytes,
+                      uint32_t n_parts, pcr_grid** out) {
+  return guarded(ctx, [&] {
+    if (!parts_device || !part_offset || !part_bytes || !out) throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    auto g = std::make_unique<pcr_grid>();
+    pcr::grid_assemble(ctx->c, static_cast<const uint8_t*>(parts_device), part_offset, part_bytes, n_parts, g->g);
+    *out = g.release();
+  });
+}
+
 int pcr_last_trace_stats(pcr_ctx* ctx, uint64_t* out5) {
   return guarded(ctx, [&] {
     uint64_t* out4 = out5;

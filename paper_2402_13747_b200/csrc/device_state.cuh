@@ -53,6 +53,7 @@ struct GridDev {
   double sub_edge = 0, sub_radius = 0, voxel_radius = 0, hit_eps = 0;
   uint64_t n_cells = 0, n_ies = 0, n_pidx = 0;
   bool march_ok = false;  // cells[].z holds compute_march_distances' values (set by it)
+  uint32_t part_voxel_lo = 0, part_voxel_hi = 0;  // a sharded build's part: its voxel range
   DBuf<int4> cells;
   DBuf<uint32_t> meta, label, edge, rx, voxel, sub, pidx;
   DBuf<double4> sc, rp, pp, pn, seg_s, seg_e;
@@ -131,6 +132,7 @@ struct Ctx {
   int fan_n = 0;
   DBuf<double> fan_table;  // n*6: cos phi, sin phi, sin(phi+dphi/2), cos(phi+dphi/2), sin(phi-dphi/2), cos(phi-dphi/2)
   int sm_count = 148;
+  std::unique_ptr<GridDev> grid_part;  // the last pcr_grid_part_build's part
   // work counters of the last pcr_propagate call (cone traces, visibility tests, cells, IEs)
   uint64_t last_trace[5] = {0, 0, 0, 0, 0};
   // per-kernel CUDA-event timing (pcr_set_profiling); resolved lazily
@@ -191,8 +193,18 @@ inline void Ctx::resolve_timers() {
 }
 
 // stage 1 (voxelize.cu)
+// one shard of a sharded build_grid: the shard's voxel range, its points'
+// surface IEs and its edge pieces / receivers; the part has no cells (assembled grid)
+struct VoxelShard {
+  uint32_t index, n_shards;
+};
 void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int division_factor,
-                       uint64_t max_cells, GridDev& out);
+                       uint64_t max_cells, GridDev& out, const VoxelShard* shard = nullptr);
 void compute_march_distances_device(Ctx& ctx, GridDev& grid);
+// grid parts (one per shard, in shard order) as bytes -> the whole grid
+uint64_t grid_part_bytes(const GridDev& part);
+void grid_part_serialize(Ctx& ctx, const GridDev& part, void* dst_device);
+void grid_assemble(Ctx& ctx, const uint8_t* parts_device, const uint64_t* offset, const uint64_t* bytes,
+                   uint32_t n_parts, GridDev& out);
 
 }  // namespace pcr

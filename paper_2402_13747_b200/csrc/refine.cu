@@ -958,7 +958,10 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
   const double4* __restrict__ nb_pa = g.nb_pa;
   const double4* __restrict__ nb_pb = g.nb_pb;
   const double eps = g.hit_eps;
-  const bool fast = g.fast_reject != 0;
+#ifndef PCR_FAST_REJECT
+#define PCR_FAST_REJECT 0
+#endif
+  const bool fast = PCR_FAST_REJECT && g.fast_reject != 0;
   long long c_num = cache->c_num, c_dn = cache->c_dn;
   double c_t = cache->c_t;
   uint32_t n_march = cache->n_march;
@@ -1020,7 +1023,10 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
     }
     carry = __shfl_sync(kFull, o, 31);
     // rounds without a hit (every record pruned or missed) leave the owners' bests as they are
-    if (!__any_sync(kFull, t < inf)) {
+#ifndef PCR_SKIP_EMPTY
+#define PCR_SKIP_EMPTY 1
+#endif
+    if (PCR_SKIP_EMPTY && !__any_sync(kFull, t < inf)) {
       __syncwarp();
       continue;
     }
@@ -1052,6 +1058,103 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
   cache->c_t = c_t;
   cache->n_march = n_march;
 }
+
+// Owner-major variant of the same scan: the posting lanes' runs are walked one owner at
+// a time, all 32 lanes on records j0 + base + lane of that owner's run. The owner's ray
+// is warp-uniform (broadcast shared-memory loads, no per-record owner lookup), and the
+// round's winner is a plain warp (t, index) min — usually a single hit, found by a
+// ballot — instead of the packed variant's segmented reduction. Pruning uses the best
+// of the owner's earlier rounds (lower record indices), so the winner is again the
+// least distance, ties to the earliest record: the serial scan's strict-< result.
+__device__ PCR_COOP_INLINE void coop_scan_owner(int lane, uint32_t len, const GridView& g, const SceneView& s,
+                                                ScanCache* cache) {
+  ScanSlot* ws = g_slots + (threadIdx.x & ~31u);
+  const double4* __restrict__ nb_rec = g.nb_rec;
+  const double4* __restrict__ nb_pa = g.nb_pa;
+  const double4* __restrict__ nb_pb = g.nb_pb;
+  const double eps = g.hit_eps;
+  const bool fast = PCR_FAST_REJECT && g.fast_reject != 0;
+  long long c_num = cache->c_num, c_dn = cache->c_dn;
+  double c_t = cache->c_t;
+  uint32_t n_march = cache->n_march;
+  ScanSlot& me = ws[lane];
+  me.best_f = kNoRec;
+  me.pre = 0;
+  unsigned owners = __ballot_sync(kFull, len > 0);
+  const double radius = 2.0 * g.sub_edge;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  __syncwarp();
+  while (owners) {
+    const int o = __ffs(owners) - 1;
+    owners &= owners - 1;
+    const uint32_t olen = __shfl_sync(kFull, len, o);
+    const ScanSlot& sl = ws[o];
+    const V3 pv{sl.prev[0], sl.prev[1], sl.prev[2]}, dv{sl.dir[0], sl.dir[1], sl.dir[2]};
+    const V3 pq{sl.pred[0], sl.pred[1], sl.pred[2]};
+    const uint32_t j0 = sl.j0;
+    double best = 1.7976931348623157e308;
+    uint32_t best_f = kNoRec;
+    for (uint32_t base = 0; base < olen; base += 32) {
+      const uint32_t F = base + lane;
+      double t = inf;
+      if (F < olen) {
+        const uint32_t j = j0 + F;
+        const double4 r4 = ldg4(nb_rec + j);
+        const double4 pa = ldg4(nb_pa + j);
+        const V3 sc = ld3(r4);
+        const double rad = pa.w;
+        if (norm_le(sc - pq, radius + rad)) {
+          ++n_march;  // counts the reference's march_segment call
+          const double t_center = dot(sc - pv, dv);
+          const double t_lo = smax(0.0, t_center - rad);
+          double bt = best;
+          if (t_lo < bt) {
+            const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r4.w));
+            if (__builtin_expect(((w >> 32) & 1u) != 0, 1)) {  // planar records are the common case
+              const double4 pb = ldg4(nb_pb + j);
+              if (planar_candidate_at(pv, dv, ld3(pa), ld3(pb), eps, t_lo, t_center + rad, bt, c_num, c_dn, c_t,
+                                      fast))
+                t = bt;
+            } else {
+              t = march_np(pv.x, pv.y, pv.z, dv.x, dv.y, dv.z, static_cast<uint32_t>(w >> 33), g, s, bt);
+            }
+          }
+        }
+      }
+      unsigned hit = __ballot_sync(kFull, t < inf);
+      if (!hit) continue;
+      int win = __ffs(hit) - 1;
+      if (hit & (hit - 1)) {  // several hits: (t, lane) min, ties to the lower lane = lower index
+        double bt = t;
+        int bl = lane;
+        for (int off = 16; off > 0; off >>= 1) {
+          const double ot = __shfl_xor_sync(kFull, bt, off);
+          const int ol = __shfl_xor_sync(kFull, bl, off);
+          if (ot < bt || (ot == bt && ol < bl)) {
+            bt = ot;
+            bl = ol;
+          }
+        }
+        win = bl;
+      }
+      best = __shfl_sync(kFull, t, win);  // < best of the earlier rounds (pruned against it)
+      best_f = base + win;
+    }
+    if (lane == o) {
+      me.best_t = best;
+      me.best_f = best_f;
+    }
+  }
+  __syncwarp();
+  cache->c_num = c_num;
+  cache->c_dn = c_dn;
+  cache->c_t = c_t;
+  cache->n_march = n_march;
+}
+
+#ifndef PCR_SCAN_OWNER
+#define PCR_SCAN_OWNER 1
+#endif
 
 template <int D, int kMinBlocks>
 __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
@@ -1104,7 +1207,10 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
           got = reproject(prev, pred, st.nd[q].label, g, s, re, n_march);
         }
       }
-      coop_scan(lane, coop ? len : 0u, g, s, &cache);
+      if (PCR_SCAN_OWNER)
+        coop_scan_owner(lane, coop ? len : 0u, g, s, &cache);
+      else
+        coop_scan(lane, coop ? len : 0u, g, s, &cache);
       if (coop) {
         const ScanSlot& me = ws[lane];
         const V3 prev{me.prev[0], me.prev[1], me.prev[2]}, dir{me.dir[0], me.dir[1], me.dir[2]};

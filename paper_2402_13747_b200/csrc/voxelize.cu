@@ -121,6 +121,35 @@ __global__ void bin_kernel(Lattice L, const double* __restrict__ pos, const uint
   }
 }
 
+// Sharded voxelization: voxel of every point, for the per-voxel point
+// histogram (splitters) and the shard's point filter
+__global__ void voxel_of_kernel(Lattice L, const double* __restrict__ pos, uint64_t n, uint32_t* __restrict__ vox) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint32_t v, s;
+    locate(L, V3{pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]}, v, s);
+    vox[i] = v;
+  }
+}
+__global__ void voxel_hist_kernel(const uint32_t* __restrict__ vox, uint64_t n, uint32_t* __restrict__ hist) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(hist + vox[i], 1u);
+}
+__global__ void in_range_kernel(const uint32_t* __restrict__ vox, uint64_t n, uint32_t lo, uint32_t hi,
+                                uint32_t* __restrict__ flag) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    flag[i] = vox[i] >= lo && vox[i] < hi;
+}
+// the shard's point ids, ascending (a stable compaction keeps the reference's tie order)
+__global__ void compact_ids_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, uint64_t n,
+                                   uint32_t* __restrict__ ids) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    if (flag[i]) ids[pos[i]] = static_cast<uint32_t>(i);
+}
+
 __global__ void gather_label_key_kernel(const uint32_t* __restrict__ label, const uint32_t* __restrict__ perm,
                                         uint64_t n, uint64_t* __restrict__ out) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -615,14 +644,14 @@ void compute_march_distances_device(Ctx& ctx, GridDev& grid) {
 }
 
 void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int division_factor,
-                       uint64_t max_cells, GridDev& out) {
+                       uint64_t max_cells, GridDev& out, const VoxelShard* shard) {
   cudaStream_t s = ctx.stream;
   // voxel_grid.cpp:83-84
   if (!(voxel_size > 0.0)) throw Error(1, "voxel_size must be > 0");
   if (division_factor < 1) throw Error(1, "division_factor must be >= 1");
 
   // ---- K1: scene_bounds(scene, voxel_size) (scene.cpp:93-106)
-  const uint64_t N = scene.n_points;
+  uint64_t N = scene.n_points;  // this build's points (a shard's subset when sharded)
   double mn[3], mx[3];
   for (int a = 0; a < 3; ++a) {
     mn[a] = std::numeric_limits<double>::max();
@@ -694,6 +723,61 @@ void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int d
   const int label_bits = bit_width(max_label);
   const bool with_label = voxel_bits + sub_bits + label_bits <= 64;
 
+  // ---- sharded build: this shard's contiguous voxel range, its points only
+  DBuf<uint32_t> shard_ids;
+  uint32_t v_lo = 0, v_hi = static_cast<uint32_t>(n_cells);
+  if (shard) {
+    if (shard->n_shards == 0 || shard->index >= shard->n_shards) throw Error(1, "voxelize: shard index out of range");
+    DBuf<uint32_t> vox(N ? N : 1, s);
+    if (N) {
+      count_launch();
+      voxel_of_kernel<<<blocks_for(N, kThreads), kThreads, 0, s>>>(L, scene.pos.get(), N, vox.get());
+      PCR_LAUNCH_CHECK();
+    }
+    // splitters: voxel ranges of about N / n_shards points each (every shard computes
+    // the same histogram of the same replicated scene, so they agree without a message)
+    {
+      DBuf<uint32_t> hist(n_cells ? n_cells : 1, s), pre(n_cells ? n_cells : 1, s), tot(1, s);
+      PCR_CUDA(cudaMemsetAsync(hist.get(), 0, sizeof(uint32_t) * (n_cells ? n_cells : 1), s));
+      if (N) {
+        count_launch();
+        voxel_hist_kernel<<<blocks_for(N, kThreads), kThreads, 0, s>>>(vox.get(), N, hist.get());
+        PCR_LAUNCH_CHECK();
+      }
+      exclusive_scan_u32(hist.get(), pre.get(), n_cells, tot.get(), s);
+      std::vector<uint32_t> hp(n_cells);
+      d2h(hp.data(), pre.get(), n_cells, s);
+      PCR_CUDA(cudaStreamSynchronize(s));
+      auto split = [&](uint32_t r) -> uint32_t {  // first voxel whose prefix reaches r N / n
+        if (r == 0) return 0;
+        if (r >= shard->n_shards) return static_cast<uint32_t>(n_cells);
+        const uint64_t want = (N * r + shard->n_shards - 1) / shard->n_shards;
+        return static_cast<uint32_t>(std::lower_bound(hp.begin(), hp.end(), want) - hp.begin());
+      };
+      v_lo = split(shard->index);
+      v_hi = std::max(v_lo, split(shard->index + 1));
+    }
+    DBuf<uint32_t> flag(N ? N : 1, s), fpos(N ? N : 1, s), cnt(1, s);
+    uint32_t n_in = 0;
+    if (N) {
+      count_launch();
+      in_range_kernel<<<blocks_for(N, kThreads), kThreads, 0, s>>>(vox.get(), N, v_lo, v_hi, flag.get());
+      PCR_LAUNCH_CHECK();
+      exclusive_scan_u32(flag.get(), fpos.get(), N, cnt.get(), s);
+      d2h(&n_in, cnt.get(), 1, s);
+      PCR_CUDA(cudaStreamSynchronize(s));
+    }
+    shard_ids.alloc(n_in ? n_in : 1, s);
+    if (n_in) {
+      count_launch();
+      compact_ids_kernel<<<blocks_for(N, kThreads), kThreads, 0, s>>>(flag.get(), fpos.get(), N, shard_ids.get());
+      PCR_LAUNCH_CHECK();
+    }
+    N = n_in;
+    out.part_voxel_lo = v_lo;
+    out.part_voxel_hi = v_hi;
+  }
+
   // ---- K2/K3: keys + stable radix sort
   DBuf<uint64_t> key(N ? N : 1, s);
   DBuf<uint32_t> sidx(N ? N : 1, s);
@@ -704,7 +788,10 @@ void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int d
   DBuf<uint32_t> n_surf_dev(1, s);
   uint32_t n_surf = 0;
   if (N) {
-    iota_u32(sidx.get(), N, s);
+    if (shard)
+      PCR_CUDA(cudaMemcpyAsync(sidx.get(), shard_ids.get(), N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    else
+      iota_u32(sidx.get(), N, s);
     if (!with_label) {
       // Keys too wide for one word: stable pass on the label first (LSD order).
       count_launch();
@@ -715,8 +802,8 @@ void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int d
     }
     count_launch();
     bin_kernel<<<blocks_for(N, kThreads), kThreads, 0, s>>>(L, scene.pos.get(), scene.label.get(),
-                                                            with_label ? nullptr : sidx.get(), N, sub_bits,
-                                                            label_bits, with_label, key.get());
+                                                            (with_label && !shard) ? nullptr : sidx.get(), N,
+                                                            sub_bits, label_bits, with_label, key.get());
     PCR_LAUNCH_CHECK();
     radix_sort_pairs(key.get(), sidx.get(), N, 0,
                      with_label ? voxel_bits + sub_bits + label_bits : voxel_bits + sub_bits, s);
@@ -771,7 +858,7 @@ void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int d
     d2h(&n_pieces, tot.get(), 1, s);
     PCR_CUDA(cudaStreamSynchronize(s));
   }
-  const uint32_t n_extra = n_pieces + n_rx;
+  uint32_t n_extra = n_pieces + n_rx;
   DBuf<ExtraIE> extra(n_extra ? n_extra : 1, s), extra_sorted(n_extra ? n_extra : 1, s);
   DBuf<uint64_t> extra_keys(n_extra ? n_extra : 1, s);
   if (n_pieces) {
@@ -791,6 +878,17 @@ void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int d
     count_launch();
     extra_rank_kernel<<<blocks_for(n_extra, 128, 1u << 30), 128, 0, s>>>(extra.get(), n_extra, extra_sorted.get());
     PCR_LAUNCH_CHECK();
+    if (shard) {  // the shard keeps the edge pieces and receivers of its voxel range (few)
+      std::vector<ExtraIE> h(n_extra), k;
+      d2h(h.data(), extra_sorted.get(), n_extra, s);
+      PCR_CUDA(cudaStreamSynchronize(s));
+      for (const ExtraIE& x : h)
+        if (x.voxel >= v_lo && x.voxel < v_hi) k.push_back(x);
+      n_extra = static_cast<uint32_t>(k.size());
+      if (n_extra) h2d(extra_sorted.get(), k.data(), n_extra, s);
+    }
+  }
+  if (n_extra) {
     count_launch();
     extract_keys_kernel<<<blocks_for(n_extra, 128, 1u << 30), 128, 0, s>>>(extra_sorted.get(), n_extra,
                                                                            extra_keys.get());
@@ -818,6 +916,11 @@ void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int d
         L, voxel_size, radius, extra_sorted.get(), n_extra, t_key.get(), n_surf, scene.rx_pos.get(),
         scene.rx_id.get(), n_rx, fo);
     PCR_LAUNCH_CHECK();
+  }
+  if (shard) {  // a part: cells and march distances come with the assembled grid
+    out.cells.release();
+    PCR_CUDA(cudaStreamSynchronize(s));
+    return;
   }
   if (n_ies) {
     count_launch();

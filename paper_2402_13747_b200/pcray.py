@@ -57,6 +57,9 @@ def lib():
         L.pcr_propagate.argtypes = [vp, vp, vp, C.c_uint32, pp(abi.InitialHits), pp(abi.TraceParams),
                                     pp(pp(abi.Paths))]
         L.pcr_last_trace_stats.argtypes = [vp, pp(C.c_uint64)]
+        L.pcr_grid_part_build.argtypes = [vp, vp, pp(abi.VoxelParams), C.c_uint32, C.c_uint32, pp(C.c_uint64)]
+        L.pcr_grid_part_copy.argtypes = [vp, vp]
+        L.pcr_grid_assemble.argtypes = [vp, vp, pp(C.c_uint64), pp(C.c_uint64), C.c_uint32, pp(vp)]
         pd, pu32, pu8 = pp(C.c_double), pp(C.c_uint32), pp(C.c_uint8)
         L.pcr_estimate_surface_batch.argtypes = [vp, vp, vp, pd, pu32, C.c_uint64, pd, pd, pd, pd]
         L.pcr_march_segment_batch.argtypes = [vp, vp, vp, pd, pd, pu32, pd, C.c_uint64, pu8, pd, pd, pu32, pd]
@@ -125,7 +128,7 @@ EXPORTED_SYMBOLS = [
     "pcr_run_pipeline", "pcr_last_trace_stats", "pcr_estimate_surface_batch", "pcr_march_segment_batch",
     "pcr_project_to_surface_batch", "pcr_local_frame_batch", "pcr_cone_intersects_sphere_batch",
     "pcr_reflect_ray_batch", "pcr_diffract_rays", "pcr_free_rays", "pcr_make_path_state", "pcr_path_eval_batch",
-    "pcr_reception_point_batch",
+    "pcr_reception_point_batch", "pcr_grid_part_build", "pcr_grid_part_copy", "pcr_grid_assemble",
 ]
 
 
@@ -254,6 +257,28 @@ def build_grid(scene, params: VoxelParams | None = None) -> DeviceGrid:
     h = C.c_void_p()
     ds.ctx.check(lib().pcr_build_grid(ds.ctx.handle, ds.handle, C.byref(params), C.byref(h)))
     return DeviceGrid(h, ds.ctx)
+
+
+def grid_part_build(scene: DeviceScene, shard: int, n_shards: int, params: VoxelParams | None = None) -> int:
+    """Sharded build_grid: this shard's part on the scene's context; its size in bytes."""
+    params = params or voxel_params()
+    nb = C.c_uint64()
+    scene.ctx.check(lib().pcr_grid_part_build(scene.ctx.handle, scene.handle, C.byref(params), shard, n_shards,
+                                              C.byref(nb)))
+    return int(nb.value)
+
+
+def grid_part_copy(ctx: Context, dst_ptr: int) -> None:
+    ctx.check(lib().pcr_grid_part_copy(ctx.handle, C.c_void_p(dst_ptr)))
+
+
+def grid_assemble(ctx: Context, parts_ptr: int, offsets, sizes) -> DeviceGrid:
+    """The grid from every shard's part (device bytes at parts_ptr + offsets[r], shard order)."""
+    off = (C.c_uint64 * len(offsets))(*[int(x) for x in offsets])
+    nb = (C.c_uint64 * len(sizes))(*[int(x) for x in sizes])
+    h = C.c_void_p()
+    ctx.check(lib().pcr_grid_assemble(ctx.handle, C.c_void_p(parts_ptr), off, nb, len(sizes), C.byref(h)))
+    return DeviceGrid(h, ctx)
 
 
 def compute_march_distances(grid: DeviceGrid) -> None:

@@ -121,6 +121,44 @@ def run_pipeline_sharded(scene: pcray.DeviceScene, config: abi.RunConfig | None 
     return pcray.shard_finish(ctx, all_outs.data_ptr() if all_outs.numel() else 0, all_outs.numel() // ob, totals)
 
 
+def build_grid_sharded(scene: pcray.DeviceScene, params=None, group=None) -> pcray.DeviceGrid:
+    """build_grid across the ranks of `group`: every rank holds the scene,
+    builds the part of its voxel range (about N / world points), the parts are
+    all-gathered (NCCL: device to device over NVLink) and every rank assembles the
+    whole grid — the unsharded grid bit for bit."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    nb = pcray.grid_part_build(scene, rank, world, params)
+    part = torch.empty(nb, dtype=torch.uint8, device=dev)
+    pcray.grid_part_copy(scene.ctx, part.data_ptr())
+    sizes = [torch.zeros(1, dtype=torch.int64, device=dev if dist.get_backend(group) != "gloo" else "cpu")
+             for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([nb], dtype=torch.int64, device=sizes[0].device), group=group)
+    sizes = [int(x.item()) for x in sizes]
+    allp = all_gather_bytes(part, group)
+    torch.cuda.current_stream().synchronize()
+    offsets = np.concatenate([[0], np.cumsum(sizes)[:-1]]).tolist()
+    return pcray.grid_assemble(scene.ctx, allp.data_ptr(), offsets, sizes)
+
+
+def build_grid_sharded_local(scene, params=None, n_shards: int = 2, device: int = 0) -> pcray.DeviceGrid:
+    """All shards of build_grid_sharded in one process on one GPU, one after another,
+    the parts concatenated on the device (proves the split exact without more GPUs)."""
+    dev = torch.device("cuda", device)
+    ds = scene if isinstance(scene, pcray.DeviceScene) else pcray.DeviceScene(scene, pcray.Context(device))
+    parts, sizes = [], []
+    for r in range(n_shards):
+        nb = pcray.grid_part_build(ds, r, n_shards, params)
+        t = torch.empty(nb, dtype=torch.uint8, device=dev)
+        pcray.grid_part_copy(ds.ctx, t.data_ptr())
+        parts.append(t)
+        sizes.append(nb)
+    allp = torch.cat(parts)
+    torch.cuda.synchronize(dev)
+    offsets = np.concatenate([[0], np.cumsum(sizes)[:-1]]).tolist()
+    return pcray.grid_assemble(ds.ctx, allp.data_ptr(), offsets, sizes)
+
+
 def run_pipeline_sharded_local(scene, config: abi.RunConfig | None = None, n_shards: int = 2,
                                order=None, device: int = 0):
     """All shards of run_pipeline_sharded in one process on one GPU, one context each,
