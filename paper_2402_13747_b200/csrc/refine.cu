@@ -80,7 +80,9 @@ __device__ __forceinline__ int voxel_floor(double p, double o, double vs) {
 // division is done once per plane (cache c_num, c_dn -> c_t). Returns true and
 // lowers best_t when this IE's hit is strictly nearer.
 //
-// Fast rejection (exact): the sdf along the ray is f(t) = dot((o + t d) - pp, n), and
+// Fast rejection (exact; off by default, PCR_FAST_REJECT=1 enables it: same-box A/B on
+// C2 depth 3, refine 554-565 ms without vs 566-574 ms with — the kernel is latency-bound
+// and the extra branch costs more than the skipped endpoint tests): the sdf along the ray is f(t) = dot((o + t d) - pp, n), and
 // in exact arithmetic f(t) = dn (t - t_e) with t_e the plane crossing. The computed
 // f(t) and the computed dn (t - t*) differ by at most ~30 u (|o| + |pp| + |t|)
 // (u = 2^-53: the dot products' rounding, num and dn's rounding, the division), which
@@ -1059,8 +1061,12 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
   cache->n_march = n_march;
 }
 
-// Owner-major variant of the same scan: the posting lanes' runs are walked one owner at
-// a time, all 32 lanes on records j0 + base + lane of that owner's run. The owner's ray
+// Owner-major variant of the same scan (A/B alternative, PCR_SCAN_OWNER=1; measured
+// slower: C2 depth 3 refine 557-563 ms packed vs 715-751 ms owner-major, depth 4
+// 7.54 s vs 9.93 s, same box — runs of ~25 records leave a quarter of the lanes idle
+// and the kernel is latency-bound, so the lighter per-record code does not pay): the
+// posting lanes' runs are walked one owner at a time, all 32 lanes on records
+// j0 + base + lane of that owner's run. The owner's ray
 // is warp-uniform (broadcast shared-memory loads, no per-record owner lookup), and the
 // round's winner is a plain warp (t, index) min — usually a single hit, found by a
 // ballot — instead of the packed variant's segmented reduction. Pruning uses the best
@@ -1153,7 +1159,7 @@ __device__ PCR_COOP_INLINE void coop_scan_owner(int lane, uint32_t len, const Gr
 }
 
 #ifndef PCR_SCAN_OWNER
-#define PCR_SCAN_OWNER 1
+#define PCR_SCAN_OWNER 0
 #endif
 
 template <int D, int kMinBlocks>
