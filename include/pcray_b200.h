@@ -438,6 +438,11 @@ typedef struct pcr_shard_stats {
 } pcr_shard_stats;
 int pcr_shard_trace(pcr_ctx* ctx, const pcr_scene* scene, const pcr_run_config* config, uint32_t shard,
                     uint32_t n_shards, uint64_t* n_rows, uint64_t* row_bytes);
+/* pcr_shard_trace on a grid the caller replicated (NCCL broadcast of one part, or the
+ * sharded build's all-gathered parts: pcr_grid_assemble); the grid must outlive the
+ * context's shard calls */
+int pcr_shard_trace_grid(pcr_ctx* ctx, const pcr_scene* scene, const pcr_grid* grid, const pcr_run_config* config,
+                         uint32_t shard, uint32_t n_shards, uint64_t* n_rows, uint64_t* row_bytes);
 int pcr_shard_rows(pcr_ctx* ctx, void* dst_device);
 int pcr_shard_refine(pcr_ctx* ctx, const pcr_scene* scene, const void* rows_device, uint64_t n_rows,
                      uint64_t* n_out, uint64_t* out_row_bytes);

@@ -461,6 +461,14 @@ int pcr_shard_trace(pcr_ctx* ctx, const pcr_scene* scene, const pcr_run_config* 
   });
 }
 
+int pcr_shard_trace_grid(pcr_ctx* ctx, const pcr_scene* scene, const pcr_grid* grid, const pcr_run_config* config,
+                         uint32_t shard, uint32_t n_shards, uint64_t* n_rows, uint64_t* row_bytes) {
+  return guarded(ctx, [&] {
+    if (!scene || !grid || !config || !n_rows || !row_bytes) throw pcr::Error(PCR_ERR_INVALID, "null argument");
+    pcr::api_shard_trace(ctx->c, scene->s, *config, shard, n_shards, n_rows, row_bytes, &grid->g);
+  });
+}
+
 int pcr_shard_rows(pcr_ctx* ctx, void* dst_device) {
   return guarded(ctx, [&] { pcr::api_shard_rows(ctx->c, dst_device); });
 }

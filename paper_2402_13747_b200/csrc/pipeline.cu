@@ -992,6 +992,8 @@ struct ShardState {
   pcr_run_config cfg{};
   uint32_t shard = 0, n_shards = 1;
   GridDev grid;
+  const GridDev* ext = nullptr;  // a grid the caller built / assembled (pcr_shard_trace_grid)
+  const GridDev& g() const { return ext ? *ext : grid; }
   std::vector<TxDev> txs;
   pcr_summary head{};  // counts and timings of this shard so far
   double trace_s = 0, refine_s = 0;
@@ -1077,7 +1079,7 @@ __global__ void unpack_outcomes_kernel(const uint8_t* __restrict__ rows, uint64_
 }  // namespace
 
 void api_shard_trace(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, uint32_t shard, uint32_t n_shards,
-                     uint64_t* n_rows, uint64_t* row_bytes) {
+                     uint64_t* n_rows, uint64_t* row_bytes, const GridDev* grid) {
   if (n_shards == 0 || shard >= n_shards) throw Error(PCR_ERR_INVALID, "shard: index out of range");
   ctx.shard = std::make_shared<ShardState>();
   ShardState& st = *ctx.shard;
@@ -1095,20 +1097,28 @@ void api_shard_trace(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg,
   stage_validate(ctx, scene);
   head_timing(S, "validate", since(t0));
   t0 = Clock::now();
-  stage_voxelize(ctx, scene, cfg, st.grid, &S);
+  if (grid) {  // replicated by the caller (NCCL broadcast or sharded build + all-gather)
+    if (grid->voxel_size != cfg.voxel_size_m || grid->dv != cfg.division_factor)
+      throw Error(PCR_ERR_INVALID, "shard: grid built with other voxel parameters");
+    st.ext = grid;
+    S.ie_count = grid->n_ies;
+    for (int a = 0; a < 3; ++a) S.grid_dims[a] = grid->dims[a];
+  } else {
+    stage_voxelize(ctx, scene, cfg, st.grid, &S);
+  }
   head_timing(S, "voxelize", since(t0));
 
   t0 = Clock::now();
   try {
     cudaStream_t s = ctx.stream;
     const pcr_trace_params tp = trace_params_of(cfg);
-    stage_transmission(ctx, st.grid, scene, st.txs, &S);
+    stage_transmission(ctx, st.g(), scene, st.txs, &S);
     std::vector<CandDev> props(n_tx);
     TraceStats ts;
     uint64_t total = 0;
     for (uint32_t t = 0; t < n_tx; ++t) {
       TxDev& x = st.txs[t];
-      propagate_device(ctx, st.grid, scene, t, x.hit_ie.get(), x.hit_kind.get(), x.hit_pos.get(), x.hit_nrm.get(),
+      propagate_device(ctx, st.g(), scene, t, x.hit_ie.get(), x.hit_kind.get(), x.hit_pos.get(), x.hit_nrm.get(),
                        x.hit_inc.get(), x.n_hits, tp, props[t], ts, shard, n_shards, true);
       release_hits(x);
       total += props[t].n;
@@ -1160,7 +1170,7 @@ void api_shard_refine(Ctx& ctx, const SceneDev& scene, const void* rows, uint64_
       slices[t] = PropSlice{&merged, off, per_tx[t]};
       off += per_tx[t];
     }
-    assemble_cands(ctx, scene, st.grid, st.txs, slices, stride, st.cs);
+    assemble_cands(ctx, scene, st.g(), st.txs, slices, stride, st.cs);
     st.merged = true;
   } catch (const std::exception& e) {
     stage_fail("trace", e);
@@ -1171,7 +1181,7 @@ void api_shard_refine(Ctx& ctx, const SceneDev& scene, const void* rows, uint64_
   t0 = Clock::now();
   try {
     RefineDevOut ro;
-    refine_cands(ctx, st.grid, scene, st.cs, st.cfg, st.shard, st.n_shards, ro);
+    refine_cands(ctx, st.g(), scene, st.cs, st.cfg, st.shard, st.n_shards, ro);
     st.stats.refine_trials = ro.trials;
     st.stats.refine_marches = ro.marches;
     st.stats.refine_trial_nodes = ro.trial_nodes;

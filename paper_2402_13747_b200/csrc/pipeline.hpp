@@ -29,7 +29,7 @@ void api_load_edges(const char* path, std::vector<double>& geom, std::vector<uin
 void api_run_pipeline(Ctx& ctx, const pcr_run_files& f, const pcr_run_config& cfg, pcr_summary** out);
 // sharded pipeline (pipeline.cu)
 void api_shard_trace(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg, uint32_t shard, uint32_t n_shards,
-                     uint64_t* n_rows, uint64_t* row_bytes);
+                     uint64_t* n_rows, uint64_t* row_bytes, const GridDev* grid = nullptr);
 void api_shard_rows(Ctx& ctx, void* dst);
 void api_shard_refine(Ctx& ctx, const SceneDev& scene, const void* rows, uint64_t n_rows, uint64_t* n_out,
                       uint64_t* out_bytes);

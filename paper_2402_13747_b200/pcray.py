@@ -92,6 +92,8 @@ def lib():
         L.pcr_shard_trace.argtypes = [vp, vp, pp(abi.RunConfig), C.c_uint32, C.c_uint32, pp(C.c_uint64),
                                       pp(C.c_uint64)]
         L.pcr_shard_rows.argtypes = [vp, vp]
+        L.pcr_shard_trace_grid.argtypes = [vp, vp, vp, pp(abi.RunConfig), C.c_uint32, C.c_uint32, pp(C.c_uint64),
+                                           pp(C.c_uint64)]
         L.pcr_shard_refine.argtypes = [vp, vp, vp, C.c_uint64, pp(C.c_uint64), pp(C.c_uint64)]
         L.pcr_shard_outcomes.argtypes = [vp, vp]
         L.pcr_shard_stats_get.argtypes = [vp, pp(abi.ShardStats)]
@@ -129,6 +131,7 @@ EXPORTED_SYMBOLS = [
     "pcr_project_to_surface_batch", "pcr_local_frame_batch", "pcr_cone_intersects_sphere_batch",
     "pcr_reflect_ray_batch", "pcr_diffract_rays", "pcr_free_rays", "pcr_make_path_state", "pcr_path_eval_batch",
     "pcr_reception_point_batch", "pcr_grid_part_build", "pcr_grid_part_copy", "pcr_grid_assemble",
+    "pcr_shard_trace_grid",
 ]
 
 
