@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <atomic>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -16,7 +17,13 @@ namespace pcr {
 
 // Device-resident scene (pcr_scene). Edges and radios are also kept on the host:
 // they are tiny and the bounds / radio bookkeeping reads them there.
+inline uint64_t next_scene_uid() {
+  static std::atomic<uint64_t> n{0};
+  return ++n;
+}
+
 struct SceneDev {
+  const uint64_t uid = next_scene_uid();  // identity for caches keyed on the scene (GridDev payloads)
   uint64_t n_points = 0;
   DBuf<double> pos, nrm;  // n*3
   DBuf<uint32_t> label;
@@ -54,6 +61,11 @@ struct GridDev {
   uint64_t n_cells = 0, n_ies = 0, n_pidx = 0;
   bool march_ok = false;  // cells[].z holds compute_march_distances' values (set by it)
   uint32_t part_voxel_lo = 0, part_voxel_hi = 0;  // a sharded build's part: its voxel range
+  // staged non-planar payloads (GridView::pay_pos): built for the scene they came from
+  mutable int has_nonplanar = -1;  // unknown until first asked
+  mutable uint64_t pay_for = 0;  // SceneDev::uid the payloads were gathered from
+  mutable DBuf<double> pay_pos, pay_nrm;
+  GridView view_for(struct Ctx& ctx, const SceneDev& scene) const;
   DBuf<int4> cells;
   DBuf<uint32_t> meta, label, edge, rx, voxel, sub, pidx;
   DBuf<double4> sc, rp, pp, pn, seg_s, seg_e;

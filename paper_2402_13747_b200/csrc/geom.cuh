@@ -54,6 +54,11 @@ struct GridView {
   // exact fast rejection in the planar reprojection scan (refine.cu planar_candidate_at):
   // set when the scene's coordinates are small enough for its error bound
   int fast_reject = 0;
+  // non-planar payloads in point_indices order (positions / normals gathered once per
+  // stage call, GridDev::view_for): estimate_surface streams them instead of a dependent
+  // point_indices -> scene gather per point; null when the grid has no non-planar IE
+  const double* pay_pos = nullptr;
+  const double* pay_nrm = nullptr;
 };
 
 // Device-resident Scene (scene.hpp:38-46).
@@ -166,13 +171,20 @@ static __device__ __noinline__ SurfaceEstimate estimate_surface(const V3& x, uin
   double best_d2 = 1.7976931348623157e308;
   const uint2 r = g.ie_range[ie];
   uint32_t best = r.x;
+  const bool staged = g.pay_pos != nullptr;
   // unrolled: consecutive points' exp() chains are independent and overlap; the sums
   // still run in point order
 #pragma unroll 4
   for (uint32_t i = r.x; i < r.y; ++i) {
-    const uint32_t pi = g.point_indices[i];
-    const V3 p = load3(s.pos + 3ull * pi);
-    const V3 n = load3(s.nrm + 3ull * pi);
+    V3 p, n;
+    if (staged) {
+      p = load3(g.pay_pos + 3ull * i);
+      n = load3(g.pay_nrm + 3ull * i);
+    } else {
+      const uint32_t pi = g.point_indices[i];
+      p = load3(s.pos + 3ull * pi);
+      n = load3(s.nrm + 3ull * pi);
+    }
     const double d2 = sqnorm(x - p);
     if (d2 < best_d2) {
       best_d2 = d2;

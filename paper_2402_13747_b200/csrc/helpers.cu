@@ -293,7 +293,7 @@ int pcr_estimate_surface_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_sce
     DBuf<double> pb(3 * n + 3, s), nb(3 * n + 3, s), sd(n + 1, s), ws(n + 1, s);
     if (n) {
       count_launch();
-      estimate_surface_kernel<<<hb(n), kHT, 0, s>>>(grid->g.view(), scene->s.view(), dx.get(), di.get(), n, pb.get(),
+      estimate_surface_kernel<<<hb(n), kHT, 0, s>>>(grid->g.view_for(ctx->c, scene->s), scene->s.view(), dx.get(), di.get(), n, pb.get(),
                                                     nb.get(), sd.get(), ws.get());
       PCR_LAUNCH_CHECK();
       d2h(p_bar, pb.get(), 3 * n, s);
@@ -321,7 +321,7 @@ int pcr_march_segment_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene*
     DBuf<uint32_t> lb(n + 1, s);
     if (n) {
       count_launch();
-      march_segment_kernel<<<hb(n), kHT, 0, s>>>(grid->g.view(), scene->s.view(), o.get(), d.get(), di.get(), tm.get(),
+      march_segment_kernel<<<hb(n), kHT, 0, s>>>(grid->g.view_for(ctx->c, scene->s), scene->s.view(), o.get(), d.get(), di.get(), tm.get(),
                                                  n, h.get(), p.get(), nr.get(), lb.get(), ds.get());
       PCR_LAUNCH_CHECK();
       d2h(hit, h.get(), n, s);
@@ -348,7 +348,7 @@ int pcr_project_to_surface_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_s
     DBuf<uint32_t> lb(n + 1, s);
     if (n) {
       count_launch();
-      project_kernel<<<hb(n), kHT, 0, s>>>(grid->g.view(), scene->s.view(), dx.get(), di.get(), n, h.get(), p.get(),
+      project_kernel<<<hb(n), kHT, 0, s>>>(grid->g.view_for(ctx->c, scene->s), scene->s.view(), dx.get(), di.get(), n, h.get(), p.get(),
                                            nr.get(), lb.get());
       PCR_LAUNCH_CHECK();
       d2h(hit, h.get(), n, s);

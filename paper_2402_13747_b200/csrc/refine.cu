@@ -1164,8 +1164,9 @@ __device__ PCR_COOP_INLINE void coop_scan_owner(int lane, uint32_t len, const Gr
 
 template <int D, int kMinBlocks>
 __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
-    refine_warp_kernel(CandIn in, uint32_t n, GridView g, SceneView s, double delta, int rho, double step_size,
-                       RefOut o, uint32_t* next_cand) {
+    refine_warp_kernel(const __grid_constant__ CandIn in, uint32_t n, const __grid_constant__ GridView g,
+                       const __grid_constant__ SceneView s, double delta, int rho, double step_size,
+                       const __grid_constant__ RefOut o, uint32_t* next_cand) {
   const int lane = threadIdx.x & 31;
   ScanSlot* ws = g_slots + (threadIdx.x & ~31u);
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
@@ -1399,7 +1400,7 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
   const uint32_t step = in.step ? in.step : 1;
   const uint32_t n_sub = in.n > in.first ? (in.n - in.first + step - 1) / step : 0;
   if (!n_sub) return;
-  GridView gv = grid.view();
+  GridView gv = grid.view_for(ctx, scene);
   DBuf<double4> rr(grid.n_ies ? grid.n_ies : 1, s);
   {
     DBuf<int> nonuni(1, s);
@@ -1483,9 +1484,14 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     // Default: the warp-cooperative kernel; PCR_REFINE_MODE=1 selects the thread-per-path
     // kernel (4 blocks of 128 threads per SM, 128 registers), kept as the A/B baseline.
     const bool warp = refine_mode() == 0;
-    auto kern = in.stride <= 3 ? refine_warp_kernel<3, kWarpMinBlocks>
-                : in.stride <= 5 ? refine_warp_kernel<5, kWarpMinBlocks>
-                                 : refine_warp_kernel<kMaxDepth, kWarpMinBlocks>;
+#ifndef PCR_REFINE_D4
+#define PCR_REFINE_D4 1
+#endif
+    // depth bounds 3, 4 (the contract C2: max_interactions 4), 5 and 8
+    auto kern = in.stride <= 3                      ? refine_warp_kernel<3, kWarpMinBlocks>
+                : (PCR_REFINE_D4 && in.stride <= 4) ? refine_warp_kernel<4, kWarpMinBlocks>
+                : in.stride <= 5                    ? refine_warp_kernel<5, kWarpMinBlocks>
+                                                    : refine_warp_kernel<kMaxDepth, kWarpMinBlocks>;
     auto kern2 = in.stride <= 3 ? refine_kernel<3, 4> : in.stride <= 5 ? refine_kernel<5, 4> : refine_kernel<kMaxDepth, 4>;
 #ifdef PCR_REFINE_CARVEOUT
     if (warp)

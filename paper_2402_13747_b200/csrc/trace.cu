@@ -763,7 +763,7 @@ void transmission_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, u
     count_launch();
     {
       KTimer kt(ctx, "transmission");
-      transmission_kernel<<<walk_blocks(n, ctx.sm_count), 128, 0, s>>>(grid.view(), scene.view(), tx,
+      transmission_kernel<<<walk_blocks(n, ctx.sm_count), 128, 0, s>>>(grid.view_for(ctx, scene), scene.view(), tx,
                                                      TxOut{los.get(), hit.get(), hp.get(), hn.get(), hi.get()});
     }
     PCR_LAUNCH_CHECK();
@@ -910,7 +910,7 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
   if (p.max_interactions > kMaxDepth) throw Error(1, "trace: max_interactions above the supported 8");
   if (p.max_diffractions >= 1 || true) ensure_fan(ctx, std::max(1, c.fan_n));
   const FanTable fan{ctx.fan_table.get(), c.fan_n};
-  const GridView gv = grid.view();
+  const GridView gv = grid.view_for(ctx, scene);
   const SceneView sv = scene.view();
 
   KeyLayout L;
@@ -1433,7 +1433,7 @@ void api_cone_trace_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, 
     rays_from_desc_kernel<<<nb(n_rays), kT, 0, s>>>(desc.get(), n_rays, rays.get());
     PCR_LAUNCH_CHECK();
   }
-  const GridView gv = grid.view();
+  const GridView gv = grid.view_for(ctx, scene);
   const SceneView sv = scene.view();
   size_t cap = std::max<size_t>(1024, 64 * m);
   DBuf<Task> tasks(cap, s);
@@ -1590,7 +1590,7 @@ void api_segment_visible_batch(Ctx& ctx, const GridDev& grid, const SceneDev& sc
   h2d(t.get(), target, 3 * n, s);
   h2d(ti.get(), target_ie, n, s);
   count_launch();
-  segvis_kernel<<<walk_blocks((n + 1) / 2, ctx.sm_count), 128, 0, s>>>(o.get(), t.get(), ti.get(), n, grid.view(),
+  segvis_kernel<<<walk_blocks((n + 1) / 2, ctx.sm_count), 128, 0, s>>>(o.get(), t.get(), ti.get(), n, grid.view_for(ctx, scene),
                                                                        scene.view(), vis.get());
   PCR_LAUNCH_CHECK();
   d2h(visible_out, vis.get(), n, s);

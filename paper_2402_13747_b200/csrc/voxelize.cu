@@ -607,7 +607,63 @@ __global__ void any_occupied_kernel(const int4* cells, size_t n, int* flag) {
     }
 }
 
+__global__ void any_nonplanar_kernel(const uint32_t* __restrict__ meta, uint64_t n, int* __restrict__ flag) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    if ((meta[i] & 3u) == kSurface && !((meta[i] >> 2) & 1u)) *flag = 1;
+}
+__global__ void gather_payload_kernel(const uint32_t* __restrict__ pidx, uint64_t n, const double* __restrict__ pos,
+                                      const double* __restrict__ nrm, uint64_t n_points, double* __restrict__ ppos,
+                                      double* __restrict__ pnrm) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t p = pidx[i];
+    if (p >= n_points) continue;  // a hand-built grid's index past the scene: never staged reads
+    for (int a = 0; a < 3; ++a) {
+      ppos[3 * i + a] = pos[3 * p + a];
+      pnrm[3 * i + a] = nrm[3 * p + a];
+    }
+  }
+}
+
 }  // namespace
+
+// The grid's view for kernels that evaluate the non-planar SDF on `scene`: the payload
+// positions and normals are gathered into point_indices order once (same values, same
+// order as estimate_surface's point_indices -> scene reads), when any IE is non-planar.
+GridView GridDev::view_for(Ctx& ctx, const SceneDev& scene) const {
+  GridView v = view();
+  cudaStream_t s = ctx.stream;
+  if (has_nonplanar < 0) {
+    DBuf<int> f(1, s);
+    PCR_CUDA(cudaMemsetAsync(f.get(), 0, sizeof(int), s));
+    if (n_ies) {
+      count_launch();
+      any_nonplanar_kernel<<<blocks_for(n_ies, kThreads), kThreads, 0, s>>>(meta.get(), n_ies, f.get());
+      PCR_LAUNCH_CHECK();
+    }
+    int h = 0;
+    d2h(&h, f.get(), 1, s);
+    PCR_CUDA(cudaStreamSynchronize(s));
+    has_nonplanar = h;
+  }
+#ifndef PCR_STAGE_PAYLOAD
+#define PCR_STAGE_PAYLOAD 1
+#endif
+  if (!PCR_STAGE_PAYLOAD || !has_nonplanar || !n_pidx) return v;
+  if (pay_for != scene.uid) {
+    pay_pos.alloc(3 * n_pidx, s);
+    pay_nrm.alloc(3 * n_pidx, s);
+    count_launch();
+    gather_payload_kernel<<<blocks_for(n_pidx, kThreads), kThreads, 0, s>>>(
+        pidx.get(), n_pidx, scene.pos.get(), scene.nrm.get(), scene.n_points, pay_pos.get(), pay_nrm.get());
+    PCR_LAUNCH_CHECK();
+    pay_for = scene.uid;
+  }
+  v.pay_pos = pay_pos.get();
+  v.pay_nrm = pay_nrm.get();
+  return v;
+}
 
 void compute_march_distances_device(Ctx& ctx, GridDev& grid) {
   cudaStream_t s = ctx.stream;
