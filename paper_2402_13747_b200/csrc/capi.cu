@@ -74,7 +74,8 @@ void pcr_destroy(pcr_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
   ctx->c.fan_table.release();
-  ctx->c.shard.reset();  // its buffers are freed on the context's stream
+  ctx->c.shard.reset();      // its buffers are freed on the context's stream
+  ctx->c.grid_part.reset();  // likewise the last sharded-voxelization part
   cudaStreamSynchronize(ctx->c.stream);
   cudaStreamDestroy(ctx->c.stream);
   delete ctx;
