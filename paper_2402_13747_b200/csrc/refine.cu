@@ -1061,6 +1061,151 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
   cache->n_march = n_march;
 }
 
+// Prefetching variant of the packed scan (PCR_SCAN_PREFETCH): the same rounds of 32
+// records over the concatenated runs, but each lane copies its NEXT round's record
+// (96 bytes: the list record and its plane) into a per-lane shared-memory slot with
+// cp.async while the current round computes, so the round reads its record from shared
+// memory instead of waiting on L2. The owner of a record index is found by a binary
+// search over the lanes' inclusive run ends (warp shuffles), which needs no per-round
+// owner map. Winners, pruning and the segmented (t, index) min are the packed scan's.
+__shared__ double4 g_pf[2][kRefineThreads][3];
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+// owning lane of concatenated record F: the first lane whose inclusive run end exceeds F
+__device__ __forceinline__ int owner_of(uint32_t F, uint32_t incl) {
+  int lo = 0, hi = 31;
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const int mid = (lo + hi) >> 1;
+    const uint32_t v = __shfl_sync(kFull, incl, mid);
+    if (v > F) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+__device__ PCR_COOP_INLINE void coop_scan_pf(int lane, uint32_t len, const GridView& g, const SceneView& s,
+                                             ScanCache* cache) {
+  const uint32_t wb = threadIdx.x & ~31u;
+  ScanSlot* ws = g_slots + wb;
+  const double4* __restrict__ nb_rec = g.nb_rec;
+  const double4* __restrict__ nb_pa = g.nb_pa;
+  const double4* __restrict__ nb_pb = g.nb_pb;
+  const double eps = g.hit_eps;
+  const bool fast = PCR_FAST_REJECT && g.fast_reject != 0;
+  long long c_num = cache->c_num, c_dn = cache->c_dn;
+  double c_t = cache->c_t;
+  uint32_t n_march = cache->n_march;
+  uint32_t incl = len;
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t v = __shfl_up_sync(kFull, incl, off);
+    if (lane >= off) incl += v;
+  }
+  const uint32_t total = __shfl_sync(kFull, incl, 31);
+  const uint32_t pre = incl - len;
+  ScanSlot& me = ws[lane];
+  me.best_f = kNoRec;
+  if (total == 0) return;
+  me.best_t = 1.7976931348623157e308;
+  me.pre = pre;
+  __syncwarp();
+  const double radius = 2.0 * g.sub_edge;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  // issue the copy of record F into buffer b (lanes past the end copy nothing)
+  auto prefetch = [&](uint32_t F, int b) {
+    const int po = owner_of(F < total ? F : total - 1, incl);  // warp-uniform shuffles
+    if (F < total) {
+      const ScanSlot& sl = ws[po];
+      const uint32_t j = sl.j0 + (F - sl.pre);
+      double4* dst = g_pf[b][threadIdx.x];
+      cp_async16(&dst[0], nb_rec + j);
+      cp_async16(reinterpret_cast<char*>(&dst[0]) + 16, reinterpret_cast<const char*>(nb_rec + j) + 16);
+      cp_async16(&dst[1], nb_pa + j);
+      cp_async16(reinterpret_cast<char*>(&dst[1]) + 16, reinterpret_cast<const char*>(nb_pa + j) + 16);
+      cp_async16(&dst[2], nb_pb + j);
+      cp_async16(reinterpret_cast<char*>(&dst[2]) + 16, reinterpret_cast<const char*>(nb_pb + j) + 16);
+    }
+    cp_async_commit();
+  };
+  prefetch(lane, 0);
+  int buf = 0;
+  for (uint32_t base = 0; base < total; base += 32) {
+    prefetch(base + 32 + lane, buf ^ 1);
+    cp_async_wait1();  // this round's record has landed
+    const uint32_t F = base + lane;
+    const bool valid = F < total;
+    const int o = owner_of(valid ? F : total - 1, incl);
+    double t = inf;
+    if (valid) {
+      const ScanSlot& sl = ws[o];
+      const double4* rec = g_pf[buf][threadIdx.x];
+      const double4 r4 = rec[0];
+      const double4 pa = rec[1];
+      const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r4.w));
+      const uint32_t ie = static_cast<uint32_t>(w >> 33);
+      const V3 sc = ld3(r4);
+      const double rad = pa.w;
+      const V3 pq{sl.pred[0], sl.pred[1], sl.pred[2]};
+      if (norm_le(sc - pq, radius + rad)) {
+        ++n_march;  // counts the reference's march_segment call
+        const V3 pv{sl.prev[0], sl.prev[1], sl.prev[2]}, dv{sl.dir[0], sl.dir[1], sl.dir[2]};
+        const double t_center = dot(sc - pv, dv);
+        const double t_lo = smax(0.0, t_center - rad);
+        double bt = sl.best_t;
+        if (t_lo < bt) {
+          if (__builtin_expect(((w >> 32) & 1u) != 0, 1)) {
+            const double4 pb = rec[2];
+            if (planar_candidate_at(pv, dv, ld3(pa), ld3(pb), eps, t_lo, t_center + rad, bt, c_num, c_dn, c_t, fast))
+              t = bt;
+          } else {
+            t = march_np(pv.x, pv.y, pv.z, dv.x, dv.y, dv.z, ie, g, s, bt);
+          }
+        }
+      }
+    }
+    buf ^= 1;
+    if (PCR_SKIP_EMPTY && !__any_sync(kFull, t < inf)) continue;
+    // segmented (t, F) min towards each owner segment's first lane in this round
+    const int ow = valid ? o : 32;
+    const int prev_o = __shfl_up_sync(kFull, ow, 1);
+    const bool head = lane == 0 || prev_o != ow;
+    const uint32_t heads = __ballot_sync(kFull, head);
+    const uint32_t above = heads & ~(kFull >> (31 - lane));
+    const int seg_end = above ? __ffs(above) - 1 : 32;
+    double bt = t;
+    uint32_t bf = F;
+    for (int off = 1; off < 32; off <<= 1) {
+      const double ot = __shfl_down_sync(kFull, bt, off);
+      const uint32_t of = __shfl_down_sync(kFull, bf, off);
+      if (lane + off < seg_end && ot < bt) {
+        bt = ot;
+        bf = of;
+      }
+    }
+    __syncwarp();
+    if (valid && head && bt < ws[o].best_t) {
+      ws[o].best_t = bt;
+      ws[o].best_f = bf;
+    }
+    __syncwarp();
+  }
+  asm volatile("cp.async.wait_all;\n" ::);
+  cache->c_num = c_num;
+  cache->c_dn = c_dn;
+  cache->c_t = c_t;
+  cache->n_march = n_march;
+}
+
+#ifndef PCR_SCAN_PREFETCH
+#define PCR_SCAN_PREFETCH 1
+#endif
+
 // Owner-major variant of the same scan (A/B alternative, PCR_SCAN_OWNER=1; measured
 // slower: C2 depth 3 refine 557-563 ms packed vs 715-751 ms owner-major, depth 4
 // 7.54 s vs 9.93 s, same box — runs of ~25 records leave a quarter of the lanes idle
@@ -1216,6 +1361,8 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
       }
       if (PCR_SCAN_OWNER)
         coop_scan_owner(lane, coop ? len : 0u, g, s, &cache);
+      else if (PCR_SCAN_PREFETCH)
+        coop_scan_pf(lane, coop ? len : 0u, g, s, &cache);
       else
         coop_scan(lane, coop ? len : 0u, g, s, &cache);
       if (coop) {
