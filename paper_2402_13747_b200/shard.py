@@ -160,7 +160,7 @@ def build_grid_sharded_local(scene, params=None, n_shards: int = 2, device: int 
 
 
 def run_pipeline_sharded_local(scene, config: abi.RunConfig | None = None, n_shards: int = 2,
-                               order=None, device: int = 0):
+                               order=None, device: int = 0, times: dict | None = None):
     """All shards of run_pipeline_sharded in one process on one GPU, one context each,
     run one after another (no shard waits on another): the exchange is a device-side
     concatenation in `order` (default rank order). Used to prove the split exact
@@ -171,8 +171,16 @@ def run_pipeline_sharded_local(scene, config: abi.RunConfig | None = None, n_sha
     ctxs = [pcray.Context(device) for _ in range(n_shards)]
     scenes = [pcray.DeviceScene(scene, c) for c in ctxs]
     rows, rb = [], 0
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    t_trace, t_refine = [], []
     for r in range(n_shards):
+        stream = torch.cuda.ExternalStream(pcray.stream_ptr(ctxs[r]))
+        a, b = ev(), ev()
+        a.record(stream)
         n, rb = pcray.shard_trace(scenes[r], config, r, n_shards)
+        b.record(stream)
+        b.synchronize()
+        t_trace.append(a.elapsed_time(b) / 1e3)
         t = _rows_tensor(n, rb, dev)
         if n:
             pcray.shard_rows(ctxs[r], t.data_ptr())
@@ -181,8 +189,14 @@ def run_pipeline_sharded_local(scene, config: abi.RunConfig | None = None, n_sha
     torch.cuda.synchronize(dev)  # the library reads it on its own streams
     outs, ob, totals = [], 0, np.zeros(len(abi.SHARD_STATS_FIELDS), dtype=np.uint64)
     for r in range(n_shards):
+        stream = torch.cuda.ExternalStream(pcray.stream_ptr(ctxs[r]))
+        a, b = ev(), ev()
+        a.record(stream)
         n_out, ob = pcray.shard_refine(scenes[r], all_rows.data_ptr() if all_rows.numel() else 0,
                                        all_rows.numel() // rb)
+        b.record(stream)
+        b.synchronize()
+        t_refine.append(a.elapsed_time(b) / 1e3)
         t = _rows_tensor(n_out, ob, dev)
         if n_out:
             pcray.shard_outcomes(ctxs[r], t.data_ptr())
@@ -190,5 +204,8 @@ def run_pipeline_sharded_local(scene, config: abi.RunConfig | None = None, n_sha
         totals = totals + pcray.shard_stats(ctxs[r])
     all_outs = torch.cat([outs[r] for r in order])
     torch.cuda.synchronize(dev)
+    if times is not None:  # per-shard device seconds of the trace and refine calls (load balance)
+        times["trace"] = t_trace
+        times["refine"] = t_refine
     return pcray.shard_finish(ctxs[0], all_outs.data_ptr() if all_outs.numel() else 0, all_outs.numel() // ob,
                               totals)

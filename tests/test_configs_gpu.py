@@ -88,7 +88,9 @@ def test_config_trace_and_refine_sample(oracle, big, name):
             ref_cones, _ = c.read(reset=True)
             del crg, crs
         got_c = pcray.propagate(tx, sub, dg, ds, tp)
-        assert pcray.last_trace_stats()["cone_traces"] == ref_cones
+        st = pcray.last_trace_stats()
+        assert st["cone_traces"] == ref_cones
+        assert st["libm_unresolved"] == 0  # every knife-edge cone decision certified (trace.cuh libm_le)
         assert_paths_equal(got_c, ref_c)
         if ref_c["n"]:
             compare_outcomes(pcray.refine_paths(ref_c, dg, ds), oracle.refine_batch(rg, rs, ref_c))

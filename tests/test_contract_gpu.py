@@ -79,7 +79,9 @@ def test_contract_config_per_path(gpu, name):
         los, hits = pcray.transmission_phase(t, dg, ds, tp)
         n_hits += hits["n"]
         parts += [los, pcray.propagate(t, hits, dg, ds, tp)]
-        cones += pcray.last_trace_stats()["cone_traces"]
+        st = pcray.last_trace_stats()
+        cones += st["cone_traces"]
+        assert st["libm_unresolved"] == 0  # every knife-edge cone decision certified against glibc
     assert n_hits == gold["initial_hits"]
     # the Mrays/s numerator: GPU cone traces = the reference's voxel_cone_trace calls
     assert cones == gold["cone_traces"], f"cone traces {cones} vs counting oracle {gold['cone_traces']}"
@@ -94,5 +96,6 @@ def test_contract_config_per_path(gpu, name):
     for k, v in gold["summary"].items():
         assert s[k] == v, f"{name} summary {k}: {s[k]} vs {v}"
     assert s["cone_traces"] == gold["cone_traces"]
+    assert s["libm_unresolved"] == 0
     assert s["transmission_rays"] == gold["transmission_rays"]
     digest.compare(digest.paths_digest(s["paths"], slots), gold["paths"], f"{name} final paths")
