@@ -431,42 +431,25 @@ struct Walker {
     active = true;
   }
 
-  // Returns the stepped axis, or -1 when the walk ended. The per-axis arrays are only
-  // indexed by compile-time constants (selects on the stepped axis), so the walker
-  // stays in registers instead of a runtime-indexed stack frame.
+  // Returns the stepped axis, or -1 when the walk ended.
   __device__ __forceinline__ int advance(const GridView& g) {
     if (!active) return -1;
-    int axis = 0;  // least t_next, ties to the lower axis (strict <, tracer.cpp:70-80)
-    double tn = t_next[0];
-    if (t_next[1] < tn) {
-      axis = 1;
-      tn = t_next[1];
-    }
-    if (t_next[2] < tn) {
-      axis = 2;
-      tn = t_next[2];
-    }
-    if (tn > t_end) {
+    int axis = 0;
+    if (t_next[1] < t_next[axis]) axis = 1;
+    if (t_next[2] < t_next[axis]) axis = 2;
+    if (t_next[axis] > t_end) {
       active = false;
       return -1;
     }
-    t_entry = tn;
-    bool out = false;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      if (a == axis) {
-        v[a] += step[a];
-        out = v[a] < 0 || v[a] >= g.dims[a];
-        t_next[a] += delta[a];
-      }
-    }
-    if (out) {
+    t_entry = t_next[axis];
+    v[axis] += step[axis];
+    if (v[axis] < 0 || v[axis] >= g.dims[axis]) {
       active = false;
       return -1;
     }
+    t_next[axis] += delta[axis];
     return axis;
   }
-  __device__ __forceinline__ int step_of(int axis) const { return axis == 0 ? step[0] : axis == 1 ? step[1] : step[2]; }
 };
 
 // cone_intersects_sphere (tracer.cpp:129-136)
@@ -596,11 +579,10 @@ __device__ inline bool warp_segment_visible(const V3& origin, const V3& target, 
       off[2] = lane / 9 - 1;
     } else {
       mine = lane < 9;
-      const int u = lane % 3 - 1, v = (lane / 3) % 3 - 1, st = w.step_of(axis);
-      // the far slab: the stepped axis at its step, the other two (axis+1, axis+2 mod 3) spanning u, v
-      off[0] = axis == 0 ? st : axis == 1 ? v : u;
-      off[1] = axis == 1 ? st : axis == 2 ? v : u;
-      off[2] = axis == 2 ? st : axis == 0 ? v : u;
+      const int u = lane % 3 - 1, v = (lane / 3) % 3 - 1;
+      off[axis] = w.step[axis];
+      off[(axis + 1) % 3] = u;
+      off[(axis + 2) % 3] = v;
     }
     const int nx = w.v[0] + off[0], ny = w.v[1] + off[1], nz = w.v[2] + off[2];
     int b = 0, cnt = 0;

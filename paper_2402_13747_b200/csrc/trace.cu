@@ -112,9 +112,8 @@ constexpr int kWalkThreads = 128;
 #ifndef PCR_WALK_MINB
 #define PCR_WALK_MINB 8
 #endif
-__global__ void __launch_bounds__(kWalkThreads, PCR_WALK_MINB) walk_kernel(const Ray* __restrict__ rays, uint32_t n_rays,
-                                                            const __grid_constant__ GridView g,
-                                                            const __grid_constant__ TraceCfg c, bool filter, Task* __restrict__ tasks,
+__global__ void __launch_bounds__(kWalkThreads, PCR_WALK_MINB) walk_kernel(const Ray* __restrict__ rays, uint32_t n_rays, GridView g,
+                                                            TraceCfg c, bool filter, Task* __restrict__ tasks,
                                                             uint32_t* __restrict__ n_tasks, uint32_t cap,
                                                             unsigned long long* __restrict__ stats) {
   const int lane = threadIdx.x & 31;
@@ -185,10 +184,8 @@ __device__ void spawn_reception(const Task tk, const Ray& r, const Node* __restr
 #endif
 __global__ void __launch_bounds__(128, PCR_VIS_MINB) visibility_kernel(const Task* __restrict__ tasks, uint32_t n_tasks,
                                                          const Ray* __restrict__ rays,
-                                                         const Node* __restrict__ parent_nodes,
-                                                         const __grid_constant__ GridView g,
-                                                         const __grid_constant__ SceneView s,
-                                                         const __grid_constant__ TraceCfg c, SpawnOut o) {
+                                                         const Node* __restrict__ parent_nodes, GridView g,
+                                                         SceneView s, TraceCfg c, SpawnOut o) {
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -284,9 +281,7 @@ struct TxOut {
 __device__ void transmission_hit(uint32_t i, const V3& tx, const GridView& g, const SceneView& s, TxOut& o);
 
 // one warp per IE: warp_segment_visible, then lane 0 classifies the reception
-__global__ void __launch_bounds__(128, 4) transmission_kernel(const __grid_constant__ GridView g,
-                                                               const __grid_constant__ SceneView s, V3 tx,
-                                                               TxOut o) {
+__global__ void __launch_bounds__(128, 4) transmission_kernel(GridView g, SceneView s, V3 tx, TxOut o) {
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;

@@ -142,39 +142,6 @@ __device__ __forceinline__ void cone_walk(const GridView& g, const Ray& r, OnEva
   if (n_ies) *n_ies += ies_seen;
 }
 
-// The cone walk's dedup set (SURVEY 8a design note): earlier evaluating voxels still
-// within Chebyshev distance 2 of the walk (at most 6 by monotone voxel coordinates, plus
-// the current one). Slots are addressed only by compile-time indices (a validity mask
-// instead of a compacted runtime-indexed list), so the set lives in registers.
-struct VoxelRing {
-  int x[8] = {0, 0, 0, 0, 0, 0, 0, 0}, y[8] = {0, 0, 0, 0, 0, 0, 0, 0}, z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  unsigned mask = 0;
-  // some live entry u with n in N(u): n was evaluated already
-  __device__ __forceinline__ bool covers(int nx, int ny, int nz) const {
-    bool hit = false;
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      hit |= ((mask >> k) & 1u) && abs(nx - x[k]) <= 1 && abs(ny - y[k]) <= 1 && abs(nz - z[k]) <= 1;
-    return hit;
-  }
-  // after evaluating at v: drop entries beyond distance 2 of v, insert v
-  __device__ __forceinline__ void push(int vx, int vy, int vz) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (!(abs(vx - x[k]) <= 2 && abs(vy - y[k]) <= 2 && abs(vz - z[k]) <= 2)) mask &= ~(1u << k);
-    const int slot = mask == 0xffu ? 0 : __ffs(~mask) - 1;  // never full (<= 7 live)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (k == slot) {
-        x[k] = vx;
-        y[k] = vy;
-        z[k] = vz;
-      }
-    }
-    mask |= 1u << slot;
-  }
-};
-
 // Knife-edge libm decisions. The reference decides `atan2(..) <= alpha +
 // asin(..)` (tracer.cpp:129-136, geometry.hpp:33-37) and `angle_between(na, nb) <=
 // 1e-9` (tracer.cpp:275-284) with glibc; the device evaluates the same expressions
@@ -252,7 +219,8 @@ __device__ __forceinline__ void warp_cone_walk(const GridView& g, const Ray& r, 
   const ConeConsts kc = cone_consts(half_angle, r.d);
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   const int ox = lane % 3 - 1, oy = (lane / 3) % 3 - 1, oz = lane / 9 - 1;
-  VoxelRing ring;
+  int ring[8][3];
+  int ring_n = 0;
   uint32_t cells_seen = 0, ies_seen = 0;
   Walker w;
   w.init(g, r.o, r.d, 0.0, inf);
@@ -261,7 +229,9 @@ __device__ __forceinline__ void warp_cone_walk(const GridView& g, const Ray& r, 
     const int march = here.z;
     if (here.x != here.y || march <= 1) {
       const int nx = w.v[0] + ox, ny = w.v[1] + oy, nz = w.v[2] + oz;
-      const bool valid = lane < 27 && in_bounds(g, nx, ny, nz) && !ring.covers(nx, ny, nz);
+      bool valid = lane < 27 && in_bounds(g, nx, ny, nz);
+      for (int k = 0; k < ring_n && valid; ++k)
+        if (abs(nx - ring[k][0]) <= 1 && abs(ny - ring[k][1]) <= 1 && abs(nz - ring[k][2]) <= 1) valid = false;
       int b = 0, cnt = 0;
       if (valid) {
         const uint32_t ni = linear_index(g, nx, ny, nz);
@@ -313,7 +283,28 @@ __device__ __forceinline__ void warp_cone_walk(const GridView& g, const Ray& r, 
         }
         on_ie(i, pass);
       }
-      ring.push(w.v[0], w.v[1], w.v[2]);
+      // dedup ring: keep earlier evaluating voxels within Chebyshev distance 2
+      int m = 0;
+      for (int k = 0; k < ring_n; ++k) {
+        if (abs(w.v[0] - ring[k][0]) <= 2 && abs(w.v[1] - ring[k][1]) <= 2 && abs(w.v[2] - ring[k][2]) <= 2) {
+          ring[m][0] = ring[k][0];
+          ring[m][1] = ring[k][1];
+          ring[m][2] = ring[k][2];
+          ++m;
+        }
+      }
+      if (m == 8) {
+        for (int k = 0; k < 7; ++k) {
+          ring[k][0] = ring[k + 1][0];
+          ring[k][1] = ring[k + 1][1];
+          ring[k][2] = ring[k + 1][2];
+        }
+        m = 7;
+      }
+      ring[m][0] = w.v[0];
+      ring[m][1] = w.v[1];
+      ring[m][2] = w.v[2];
+      ring_n = m + 1;
     }
     if (march >= 2) {
       w.init(g, r.o, r.d, w.t_entry + static_cast<double>(march - 1) * g.voxel_size, inf);
