@@ -377,6 +377,78 @@ __device__ __forceinline__ bool same_snapshot(const Snapshot<D>& sn, const RNode
   return true;
 }
 
+// Cycle detection without keeping the last states: a 64-bit hash of every post-iteration
+// state is compared with the hashes of the states 1 and 2 iterations back and of
+// Brent's saved state (taken at power-of-two steps). A hash match only SCHEDULES an
+// exact check: the matching state S_i is copied and compared bitwise with S_{i+p},
+// p being the suspected period. S_{i+p} == S_i means the trajectory repeats with
+// period p from i, every state of the cycle has already failed ||g|| < delta, and the
+// reference iterates to rho and reports not_converged — so the exit is exact whatever
+// the hash did. One snapshot instead of three, and no snapshot store per iteration.
+__device__ __forceinline__ uint64_t mix64(uint64_t h, uint64_t w) {
+  h ^= w;
+  h *= 0x9e3779b97f4a7c15ull;
+  return h ^ (h >> 29);
+}
+template <int D>
+__device__ __forceinline__ uint64_t state_hash(const RNode* nd, int d) {
+  uint64_t h = 0x243f6a8885a308d3ull;
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    if (q >= d) break;
+    if (nd[q].kind == 0) {
+      h = mix64(h, static_cast<uint64_t>(__double_as_longlong(nd[q].c.x)));
+      h = mix64(h, static_cast<uint64_t>(__double_as_longlong(nd[q].c.y)));
+      h = mix64(h, static_cast<uint64_t>(__double_as_longlong(nd[q].c.z)));
+      h = mix64(h, static_cast<uint64_t>(__double_as_longlong(nd[q].n.x)));
+      h = mix64(h, static_cast<uint64_t>(__double_as_longlong(nd[q].n.y)));
+      h = mix64(h, static_cast<uint64_t>(__double_as_longlong(nd[q].n.z)));
+      h = mix64(h, nd[q].label);
+    } else {
+      h = mix64(h, static_cast<uint64_t>(__double_as_longlong(nd[q].p0)));
+    }
+  }
+  return h;
+}
+template <int D>
+struct CycleCheck {
+  uint64_t h1, h2, hs;   // hashes of S_{i-1}, S_{i-2} and of Brent's saved state
+  int saved_iter, power, lam, pend_at;
+  Snapshot<D> pending;   // a state suspected to recur at iteration pend_at
+  __device__ __forceinline__ void init(const RNode* nd, int d) {
+    h1 = h2 = hs = state_hash<D>(nd, d);
+    saved_iter = -1;
+    power = 1;
+    lam = 0;
+    pend_at = -1;
+  }
+  // after iteration i produced the state nd: true when the trajectory is periodic
+  __device__ __forceinline__ bool periodic(const RNode* nd, int d, int i) {
+    const uint64_t h = state_hash<D>(nd, d);
+    bool cyc = false;
+    if (pend_at == i) {
+      cyc = same_snapshot(pending, nd, d);  // the exact test
+      pend_at = -1;
+    }
+    if (!cyc && pend_at < 0) {
+      const int p = h == h1 ? 1 : h == h2 ? 2 : h == hs ? i - saved_iter : 0;
+      if (p > 0) {
+        take_snapshot(pending, nd, d);
+        pend_at = i + p;
+      }
+    }
+    h2 = h1;
+    h1 = h;
+    if (++lam == power) {
+      hs = h;
+      saved_iter = i;
+      power <<= 1;
+      lam = 0;
+    }
+    return cyc;
+  }
+};
+
 template <int D>
 __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const GridView& g, const SceneView& s,
                                            double delta, int rho, double step_size, const RefOut& o);
@@ -467,12 +539,9 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
     atomicAdd(o.stats + 2, static_cast<unsigned long long>(n_trials) * d);
     atomicAdd(o.stats + 3, static_cast<unsigned long long>(n_iter_nodes));
   };
-  // Brent cycle detection on the post-iteration state
-  Snapshot<D> saved, last[2];  // Brent's saved state; the states 1 and 2 iterations back
-  take_snapshot(saved, nd, d);
-  last[0] = saved;
-  last[1] = saved;
-  int power = 1, lam = 0;
+  // cycle detection on the post-iteration state (CycleCheck)
+  CycleCheck<D> cyc;
+  cyc.init(nd, d);
   bool stalled = false;
   for (; iter < rho; ++iter) {
     n_iter_nodes += d;
@@ -559,18 +628,10 @@ __device__ __forceinline__ void refine_one(uint32_t k, const CandIn& in, const G
     }
     for (int q = 0; q < d; ++q) pts[q] = node_point(nd[q], nd[q].p0, nd[q].p1);
     f = chain_len(tx, pts, d, rx);
-    // periodic trajectory: never converges (see Snapshot). Periods 1 and 2 are caught
-    // at once, longer ones by Brent's doubling schedule.
-    const int slot = iter & 1;
-    if (same_snapshot(last[slot ^ 1], nd, d) || same_snapshot(last[slot], nd, d) || same_snapshot(saved, nd, d)) {
+    // periodic trajectory: never converges (see Snapshot / CycleCheck)
+    if (cyc.periodic(nd, d, iter)) {
       stalled = true;
       break;
-    }
-    take_snapshot(last[slot], nd, d);
-    if (++lam == power) {
-      saved = last[slot];
-      power <<= 1;
-      lam = 0;
     }
   }
   o.iters[k] = static_cast<uint32_t>(converged || stalled ? iter + 1 : iter);  // iterations executed
@@ -643,12 +704,12 @@ struct RunCache {
 template <int D>
 struct PathState {
   uint32_t k;
-  int d, iter, power, lam;
+  int d, iter;
   V3 tx, rx;
   double f, gnorm;
   RNode nd[D];
   V3 pts[D];
-  Snapshot<D> saved, last[2];
+  CycleCheck<D> cyc;
   RunCache rc[D];
 };
 
@@ -703,11 +764,7 @@ __device__ PCR_STEP_INLINE bool path_init(PathState<D>& st, uint32_t k, const Ca
   st.f = chain_len(st.tx, st.pts, d, st.rx);
   st.gnorm = 0.0;
   st.iter = 0;
-  take_snapshot(st.saved, st.nd, d);
-  st.last[0] = st.saved;
-  st.last[1] = st.saved;
-  st.power = 1;
-  st.lam = 0;
+  st.cyc.init(st.nd, d);
   return true;
 }
 
@@ -857,18 +914,10 @@ __device__ PCR_STEP_INLINE bool path_step_c(PathState<D>& st, const RefOut& o) {
     }
   }
   st.f = len + norm(st.rx - prev);
-  const int slot = st.iter & 1;
-  if (same_snapshot(st.last[slot ^ 1], st.nd, d) || same_snapshot(st.last[slot], st.nd, d) ||
-      same_snapshot(st.saved, st.nd, d)) {
+  if (st.cyc.periodic(st.nd, d, st.iter)) {
     o.iters[st.k] = static_cast<uint32_t>(st.iter + 1);
     o.reason[st.k] = PCR_NOT_CONVERGED;
     return false;
-  }
-  take_snapshot(st.last[slot], st.nd, d);
-  if (++st.lam == st.power) {
-    st.saved = st.last[slot];
-    st.power <<= 1;
-    st.lam = 0;
   }
   ++st.iter;
   return true;
@@ -1061,7 +1110,9 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
   cache->n_march = n_march;
 }
 
-// Prefetching variant of the packed scan (PCR_SCAN_PREFETCH): the same rounds of 32
+// Prefetching variant of the packed scan (PCR_SCAN_PREFETCH=1; measured slower and off:
+// C2 depth 4 refine 7.20-7.21 s without vs 7.70-7.72 s with, depth 3 574 vs 622 ms,
+// same box — the record loads are not what the rounds wait on): the same rounds of 32
 // records over the concatenated runs, but each lane copies its NEXT round's record
 // (96 bytes: the list record and its plane) into a per-lane shared-memory slot with
 // cp.async while the current round computes, so the round reads its record from shared
@@ -1203,7 +1254,7 @@ __device__ PCR_COOP_INLINE void coop_scan_pf(int lane, uint32_t len, const GridV
 }
 
 #ifndef PCR_SCAN_PREFETCH
-#define PCR_SCAN_PREFETCH 1
+#define PCR_SCAN_PREFETCH 0
 #endif
 
 // Owner-major variant of the same scan (A/B alternative, PCR_SCAN_OWNER=1; measured
