@@ -143,7 +143,7 @@ __device__ __forceinline__ bool planar_candidate(const V3& prev, const V3& dir, 
 
 // reproject (refine.cpp:80-130) with surface_ies_near (:34-52) scanned in place.
 // first_pass = 1 skips the same-label pass (done cooperatively by refine_warp_kernel).
-__device__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, const GridView& g, const SceneView& s,
+__device__ __noinline__ bool reproject(const V3& prev, const V3& predicted, uint32_t label, const GridView& g, const SceneView& s,
                           Reproj& out, uint32_t& n_march, int first_pass = 0) {
   const V3 diff = predicted - prev;
   const double dist = norm(diff);
@@ -707,8 +707,7 @@ struct PathState {
   int d, iter;
   V3 tx, rx;
   double f, gnorm;
-  RNode nd[D];
-  V3 pts[D];
+  RNode nd[D];  // node points are recomputed from them (node_point: same bits every time)
   CycleCheck<D> cyc;
   RunCache rc[D];
 };
@@ -757,11 +756,12 @@ __device__ PCR_STEP_INLINE bool path_init(PathState<D>& st, uint32_t k, const Ca
       x.n = V3{0, 0, 1};
     }
   }
+  V3 pts[D];
   for (int q = 0; q < d; ++q) {
-    st.pts[q] = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
+    pts[q] = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
     st.rc[q].cell = 0xffffffffu;
   }
-  st.f = chain_len(st.tx, st.pts, d, st.rx);
+  st.f = chain_len(st.tx, pts, d, st.rx);
   st.gnorm = 0.0;
   st.iter = 0;
   st.cyc.init(st.nd, d);
@@ -774,9 +774,11 @@ __device__ PCR_STEP_INLINE void path_converged(const PathState<D>& st, const Can
                                const RefOut& o) {
   const uint32_t k = st.k;
   const int d = st.d;
+  V3 pts[D];
+  for (int q = 0; q < d; ++q) pts[q] = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
   V3 prev = st.tx;
   for (int q = 0; q <= d; ++q) {
-    const V3 next = q < d ? st.pts[q] : st.rx;
+    const V3 next = q < d ? pts[q] : st.rx;
     if (!segment_visible(prev, next, kNoIe, g, s)) {
       o.reason[k] = PCR_OCCLUDED;
       return;
@@ -785,13 +787,13 @@ __device__ PCR_STEP_INLINE void path_converged(const PathState<D>& st, const Can
   }
   for (int q = 0; q < d; ++q) {
     const size_t j = static_cast<size_t>(k) * in.stride + q;
-    store3(o.pos + 3 * j, st.pts[q]);
+    store3(o.pos + 3 * j, pts[q]);
     if (st.nd[q].kind == 0) {
       store3(o.nrm + 3 * j, st.nd[q].n);
       o.label[j] = st.nd[q].label;
     }
   }
-  const double total = chain_len(st.tx, st.pts, d, st.rx);
+  const double total = chain_len(st.tx, pts, d, st.rx);
   o.length[k] = total;
   o.delay[k] = total / kSpeedOfLight;
   o.gnorm[k] = st.gnorm;
@@ -821,7 +823,7 @@ __device__ PCR_STEP_INLINE bool path_step_a(PathState<D>& st, const CandIn& in, 
 #pragma unroll
   for (int q = 0; q < D; ++q) {
     if (q < d) {
-      pts[q] = st.pts[q];
+      pts[q] = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
       refl[q] = st.nd[q].kind == 0;
     }
   }
@@ -908,7 +910,6 @@ __device__ PCR_STEP_INLINE bool path_step_c(PathState<D>& st, const RefOut& o) {
   for (int q = 0; q < D; ++q) {
     if (q < d) {
       const V3 p = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
-      st.pts[q] = p;
       len += norm(p - prev);
       prev = p;
     }
