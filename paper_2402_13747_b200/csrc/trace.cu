@@ -182,7 +182,8 @@ __device__ void spawn_reception(const Task tk, const Ray& r, const Node* __restr
 #ifndef PCR_VIS_MINB
 #define PCR_VIS_MINB 8
 #endif
-__global__ void __launch_bounds__(128, PCR_VIS_MINB) visibility_kernel(const Task* __restrict__ tasks, uint32_t n_tasks,
+__global__ void __launch_bounds__(128, PCR_VIS_MINB) visibility_kernel(const Task* __restrict__ tasks,
+                                                         const uint32_t* __restrict__ n_tasks_dev, uint32_t cap,
                                                          const Ray* __restrict__ rays,
                                                          const Node* __restrict__ parent_nodes, GridView g,
                                                          SceneView s, TraceCfg c, SpawnOut o) {
@@ -192,6 +193,11 @@ __global__ void __launch_bounds__(128, PCR_VIS_MINB) visibility_kernel(const Tas
   // visible tasks are queued one per lane and spawned 32 at a time (one lane each)
   // instead of by lane 0 alone after every test; appends are atomic either way and
   // the node/candidate order is canonicalised downstream
+  // the walk's task count stays on the device (no host round trip between the two
+  // kernels); a walk that overflowed the buffer left an incomplete list: do nothing,
+  // the host sees the count and reruns the chunk with a bigger buffer
+  const uint32_t n_tasks = *n_tasks_dev;
+  if (n_tasks > cap) return;
   uint32_t mine = 0;
   int queued = 0;
   for (uint32_t t = warp; t < n_tasks; t += nwarps) {
@@ -924,7 +930,7 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
   // node arena
   size_t node_cap = std::max<size_t>(1u << 20, 2ull * n_local);
   DBuf<Node> nodes(node_cap, s);
-  DBuf<uint32_t> counters(2, s);  // n_nodes, n_cands
+  DBuf<uint32_t> counters(3, s);  // n_tasks, n_nodes, n_cands
   uint32_t n_nodes = n_local;
   count_launch();
   seed_kernel<<<nb(n_local), kT, 0, s>>>(hit_ie, hit_kind, hit_pos, hit_nrm, hit_inc, n_local, shard, n_shards, gv, sv,
@@ -985,10 +991,26 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
     PCR_CUDA(cudaMemsetAsync(alive.get(), 0, sizeof(unsigned long long), s));
     count_launch();
     count_alive_kernel<<<nb(nr), kT, 0, s>>>(rays.get(), nr, alive.get());
-    // walk -> tasks (retry with a bigger task buffer on overflow)
+    // walk -> tasks -> visibility with one host round trip: capacity for the worst case
+    // (every task spawns) is reserved up front, the visibility kernel reads the task
+    // count from the device, and an overflowing walk reruns with a bigger buffer
     uint32_t n_tasks = 0;
+    unsigned long long h_alive = 0;
+    const uint32_t before_nodes = n_nodes;
     for (;;) {
-      PCR_CUDA(cudaMemsetAsync(counters.get(), 0, sizeof(uint32_t), s));
+      if (n_nodes + task_cap > node_cap) {
+        const size_t nc = std::max(node_cap * 2, n_nodes + task_cap + (1u << 20));
+        if (nc > 0xfffffff0ull) throw Error(3, "trace: interaction arena exceeds 2^32 nodes");
+        nodes.reserve(nc, n_nodes, s);
+        node_cap = nc;
+      }
+      if (n_cands + task_cap > cand_cap) {
+        const size_t nc = std::max(cand_cap * 2, n_cands + task_cap);
+        cands.reserve(nc, n_cands, s);
+        cand_cap = nc;
+      }
+      uint32_t h_cnt[3] = {0, n_nodes, n_cands};  // tasks, nodes, candidates
+      h2d(counters.get(), h_cnt, 3, s);
       count_launch();
       {
         KTimer kt(ctx, "cone_walk");
@@ -997,48 +1019,29 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
                                                 static_cast<uint32_t>(task_cap), walk_stats.get());
       }
       PCR_LAUNCH_CHECK();
-      d2h(&n_tasks, counters.get(), 1, s);
+      count_launch();
+      {
+        KTimer kt(ctx, "visibility");
+        visibility_kernel<<<walk_blocks(task_cap, ctx.sm_count), 128, 0, s>>>(
+            tasks.get(), counters.get(), static_cast<uint32_t>(task_cap), rays.get(), nodes.get(), gv, sv, c,
+            SpawnOut{nodes.get(), counters.get() + 1, cands.get(), counters.get() + 2, nullptr});
+      }
+      PCR_LAUNCH_CHECK();
+      d2h(h_cnt, counters.get(), 3, s);
+      d2h(&h_alive, alive.get(), 1, s);
       PCR_CUDA(cudaStreamSynchronize(s));
-      if (n_tasks <= task_cap) break;
-      task_cap = static_cast<size_t>(n_tasks) * 5 / 4 + 1024;
+      n_tasks = h_cnt[0];
+      if (n_tasks <= task_cap) {
+        n_nodes = h_cnt[1];
+        n_cands = h_cnt[2];
+        break;
+      }
+      task_cap = static_cast<size_t>(n_tasks) * 5 / 4 + 1024;  // visibility did nothing: rerun the chunk
       tasks.alloc(task_cap, s);
     }
-    unsigned long long h_alive = 0;
-    d2h(&h_alive, alive.get(), 1, s);
-    if (n_tasks == 0) {
-      PCR_CUDA(cudaStreamSynchronize(s));
-      stats.cone_traces += h_alive;
-      continue;
-    }
-    // capacity for the worst case (every task spawns)
-    if (n_nodes + static_cast<size_t>(n_tasks) > node_cap) {
-      const size_t nc = std::max(node_cap * 2, n_nodes + static_cast<size_t>(n_tasks) + (1u << 20));
-      if (nc > 0xfffffff0ull) throw Error(3, "trace: interaction arena exceeds 2^32 nodes");
-      nodes.reserve(nc, n_nodes, s);
-      node_cap = nc;
-    }
-    if (n_cands + static_cast<size_t>(n_tasks) > cand_cap) {
-      const size_t nc = std::max(cand_cap * 2, n_cands + static_cast<size_t>(n_tasks));
-      cands.reserve(nc, n_cands, s);
-      cand_cap = nc;
-    }
-    const uint32_t before_nodes = n_nodes;
-    uint32_t h_cnt[2] = {n_nodes, n_cands};
-    h2d(counters.get(), h_cnt, 2, s);
-    count_launch();
-    {
-      KTimer kt(ctx, "visibility");
-      visibility_kernel<<<walk_blocks(n_tasks, ctx.sm_count), 128, 0, s>>>(
-          tasks.get(), n_tasks, rays.get(), nodes.get(), gv, sv, c,
-          SpawnOut{nodes.get(), counters.get(), cands.get(), counters.get() + 1, nullptr});
-    }
-    PCR_LAUNCH_CHECK();
-    d2h(h_cnt, counters.get(), 2, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
     stats.cone_traces += h_alive;
     stats.visibility_tests += n_tasks;
-    n_nodes = h_cnt[0];
-    n_cands = h_cnt[1];
+    if (n_tasks == 0) continue;
     if (n_cands > kappa_trigger) {
       // exact pre-cap (a subset's first-kappa is a superset of its share of the global one)
       DBuf<Cand> kept;
