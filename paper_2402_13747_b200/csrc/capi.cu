@@ -180,7 +180,7 @@ int pcr_grid_upload(pcr_ctx* ctx, const pcr_grid_host* h, pcr_grid** out) {
       G.n_pidx = h->n_point_indices;
       G.pidx.alloc(G.n_pidx ? G.n_pidx : 1, s);
       pcr::h2d(G.pidx.get(), h->point_indices, G.n_pidx, s);
-      PCR_CUDA(cudaStreamSynchronize(s));
+      pcr::stream_wait(s);
     } catch (...) {
       delete gg;
       throw;
@@ -222,7 +222,7 @@ int pcr_grid_download(pcr_ctx* ctx, const pcr_grid* grid, pcr_grid_host** out) {
       pcr::d2h(h->ie_voxel, G.voxel.get(), ni, s);
       pcr::d2h(h->ie_subvoxel, G.sub.get(), ni, s);
       pcr::d2h(h->point_indices, G.pidx.get(), G.n_pidx, s);
-      PCR_CUDA(cudaStreamSynchronize(s));
+      pcr::stream_wait(s);
       for (size_t i = 0; i < nc; ++i) {
         h->cell_ie_begin[i] = static_cast<uint32_t>(cells[i].x);
         h->cell_ie_end[i] = static_cast<uint32_t>(cells[i].y);

@@ -26,6 +26,18 @@ struct Error : std::runtime_error {
     }                                                                                           \
   } while (0)
 
+// Wait for a stream by polling it: the host loops of the trace and refine stages read a
+// few counters back per chunk, and a blocking / yielding wait can wake up milliseconds
+// late on a busy host (measured: the same C2 trace stage 1.4-3.6 s across repetitions),
+// so the library spins on cudaStreamQuery instead of sleeping in cudaStreamSynchronize.
+inline void stream_wait(cudaStream_t s) {
+  cudaError_t e;
+  while ((e = cudaStreamQuery(s)) == cudaErrorNotReady) {
+  }
+  if (e != cudaSuccess)
+    throw ::pcr::Error(e == cudaErrorMemoryAllocation ? 3 : 2, std::string("cuda stream wait: ") + cudaGetErrorString(e));
+}
+
 // Launch errors; with PCR_SYNC_LAUNCHES=1 in the environment every checked launch is
 // also synchronised, so an asynchronous fault names the kernel's source line (debug aid).
 bool sync_launches();

@@ -112,7 +112,7 @@ void grid_part_serialize(Ctx& ctx, const GridDev& p, void* dst_device) {
     PCR_CUDA(cudaMemcpyAsync(d + L.range, p.range.get(), 8 * p.n_ies, cudaMemcpyDeviceToDevice, s));
   }
   if (p.n_pidx) PCR_CUDA(cudaMemcpyAsync(d + L.pidx, p.pidx.get(), 4 * p.n_pidx, cudaMemcpyDeviceToDevice, s));
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
 }
 
 void grid_assemble(Ctx& ctx, const uint8_t* parts, const uint64_t* offset, const uint64_t* bytes, uint32_t n_parts,
@@ -124,7 +124,7 @@ void grid_assemble(Ctx& ctx, const uint8_t* parts, const uint64_t* offset, const
     if (bytes[r] < sizeof(PartHeader)) throw Error(1, "voxelize: grid part truncated");
     PCR_CUDA(cudaMemcpyAsync(&h[r], parts + offset[r], sizeof(PartHeader), cudaMemcpyDeviceToHost, s));
   }
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   uint64_t n_ies = 0, n_pidx = 0;
   for (uint32_t r = 0; r < n_parts; ++r) {
     const PartHeader& x = h[r];
@@ -178,7 +178,7 @@ void grid_assemble(Ctx& ctx, const uint8_t* parts, const uint64_t* offset, const
     PCR_LAUNCH_CHECK();
   }
   compute_march_distances_device(ctx, out);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
 }
 
 }  // namespace pcr

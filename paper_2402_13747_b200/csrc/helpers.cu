@@ -301,7 +301,7 @@ int pcr_estimate_surface_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_sce
       d2h(sdf, sd.get(), n, s);
       d2h(weight_sum, ws.get(), n, s);
     }
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
   });
 }
 
@@ -330,7 +330,7 @@ int pcr_march_segment_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scene*
       d2h(label, lb.get(), n, s);
       d2h(distance, ds.get(), n, s);
     }
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
   });
 }
 
@@ -356,7 +356,7 @@ int pcr_project_to_surface_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_s
       d2h(normal, nr.get(), 3 * n, s);
       d2h(label, lb.get(), n, s);
     }
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
   });
 }
 
@@ -377,7 +377,7 @@ int pcr_reception_point_batch(pcr_ctx* ctx, const pcr_grid* grid, const pcr_scen
       PCR_LAUNCH_CHECK();
       d2h(point, out.get(), 3 * n, s);
     }
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
   });
 }
 
@@ -394,7 +394,7 @@ int pcr_local_frame_batch(pcr_ctx* ctx, const double* normal, uint64_t n, double
       d2h(u, du.get(), 3 * n, s);
       d2h(v, dv.get(), 3 * n, s);
     }
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
   });
 }
 
@@ -411,7 +411,7 @@ int pcr_cone_intersects_sphere_batch(pcr_ctx* ctx, const double* o, const double
       PCR_LAUNCH_CHECK();
       d2h(out, res.get(), n, s);
     }
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
   });
 }
 
@@ -432,7 +432,7 @@ int pcr_reflect_ray_batch(pcr_ctx* ctx, const pcr_grid* grid, const double* hit_
       d2h(ok, dok.get(), n, s);
       d2h(rays, dr.get(), n, s);
     }
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
   });
 }
 
@@ -456,7 +456,7 @@ int pcr_diffract_rays(pcr_ctx* ctx, const pcr_scene* scene, uint32_t edge_index,
     std::vector<pcr_ray_desc> h_r(fan_n);
     d2h(h_ok.data(), dok.get(), fan_n, s);
     d2h(h_r.data(), dr.get(), fan_n, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
     uint64_t m = 0;
     for (int j = 0; j < fan_n; ++j) m += h_ok[j];
     pcr_ray_desc* out = halloc<pcr_ray_desc>(m ? m : 1);
@@ -494,7 +494,7 @@ int pcr_make_path_state(pcr_ctx* ctx, const pcr_scene* scene, const pcr_paths* c
                                             ed.get(), out.get());
     PCR_LAUNCH_CHECK();
     d2h(nodes, out.get(), n * st, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
   });
 }
 
@@ -522,7 +522,7 @@ int pcr_path_eval_batch(pcr_ctx* ctx, const double* tx, const double* rx, const 
       d2h(gradients, gr.get(), 2 * n * st, s);
       d2h(gradients_ok, gok.get(), n, s);
     }
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
   });
 }
 

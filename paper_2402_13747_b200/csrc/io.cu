@@ -294,7 +294,7 @@ void api_scene_load_ply(Ctx& ctx, const char* path, const pcr_scene_desc& rest, 
         v += rows;
         b ^= 1;
       }
-      PCR_CUDA(cudaStreamSynchronize(s));
+      stream_wait(s);
     } catch (...) {
       cudaStreamSynchronize(s);
       cudaEventDestroy(done[0]);
@@ -324,7 +324,7 @@ void api_scene_load_ply(Ctx& ctx, const char* path, const pcr_scene_desc& rest, 
     h2d(S.label.get(), lab.data(), lab.size(), s);
   }
   upload_rest(ctx, rest, S);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
 }
 
 void api_scene_points(Ctx& ctx, const SceneDev& S, double* pos, double* nrm, uint32_t* label) {
@@ -332,7 +332,7 @@ void api_scene_points(Ctx& ctx, const SceneDev& S, double* pos, double* nrm, uin
   if (pos) d2h(pos, S.pos.get(), 3 * S.n_points, s);
   if (nrm) d2h(nrm, S.nrm.get(), 3 * S.n_points, s);
   if (label) d2h(label, S.label.get(), S.n_points, s);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
 }
 
 // write_paths (io.cpp:317-349): header with the config hash, then one record per path.

@@ -83,7 +83,7 @@ bool first_violation_device(Ctx& ctx, const SceneDev& S, Violation& v) {
   std::vector<uint32_t> lh(S.n_edges + 1ull);
   d2h(&fb, first.get(), 1, s);
   d2h(lh.data(), hit.get(), lh.size(), s);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   std::vector<Violation> out;
   auto add = [&](const std::string& rule, size_t i, const std::string& detail) {
     if (out.empty()) out.push_back({rule, detail, i});
@@ -92,7 +92,7 @@ bool first_violation_device(Ctx& ctx, const SceneDev& S, Violation& v) {
     double p[3], q[3];
     d2h(p, S.pos.get() + 3 * fb, 3, s);
     d2h(q, S.nrm.get() + 3 * fb, 3, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
     if (!(std::isfinite(p[0]) && std::isfinite(p[1]) && std::isfinite(p[2])))
       add("point_position_finite", fb, "non-finite position");
     const double nn = norm(load3(q));
@@ -263,7 +263,7 @@ void upload_scene(Ctx& ctx, const pcr_scene_desc& d, SceneDev& S) {
   h2d(S.rx_pos.get(), S.h_rx.data(), S.h_rx.size(), s);
   h2d(S.rx_id.get(), S.h_rx_id.data(), S.h_rx_id.size(), s);
   S.carrier_frequency_hz = d.carrier_frequency_hz;
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
 }
 
 void api_run_pipeline_on_scene(Ctx& ctx, const pcr_scene_desc& desc, const pcr_run_config& cfg, pcr_summary** out) {
@@ -439,7 +439,7 @@ void assemble_cands(Ctx& ctx, const SceneDev& scene, const GridDev& grid, const 
       row += p.n;
     }
   }
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
 }
 
 void refine_cands(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const CandSet& cs, const pcr_run_config& cfg,
@@ -737,7 +737,7 @@ std::vector<uint32_t> group_by(Ctx& ctx, const ExactView& v, DBuf<uint32_t>& ord
   int c = 0;
   d2h(&ng, tot.get(), 1, s);
   d2h(&c, coll.get(), 1, s);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   if (c) throw Error(4, "dedup: group hash collision");
   heads.alloc(ng ? ng : 1, s);
   if (m) {
@@ -770,7 +770,7 @@ std::vector<EP> dedup_device(Ctx& ctx, const CandSet& cs, const RefineDevOut& ro
   unsigned long long hc[5];
   d2h(&m, tot.get(), 1, s);
   d2h(hc, counts.get(), 5, s);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   for (int r = 0; r < 4; ++r) S->rejected[r] = hc[r];
   S->refine_iterations = hc[4];
   S->refined_paths = m;
@@ -824,7 +824,7 @@ std::vector<EP> dedup_device(Ctx& ctx, const CandSet& cs, const RefineDevOut& ro
     PCR_LAUNCH_CHECK();
     exclusive_scan_u32(f2.get(), p2.get(), ng, t2.get(), s);
     d2h(&mf, t2.get(), 1, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
     fin.alloc(mf ? mf : 1, s);
     count_launch();
     compact_idx_kernel<<<nb(ng), 256, 0, s>>>(f2.get(), p2.get(), ng, kept.get(), fin.get());
@@ -842,7 +842,7 @@ std::vector<EP> dedup_device(Ctx& ctx, const CandSet& cs, const RefineDevOut& ro
   d2h(ids.data(), fin.get(), mf, s);
   std::vector<uint32_t> hsrc(m);
   d2h(hsrc.data(), src.get(), m, s);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   const uint32_t stv = cs.stride;
   std::vector<EP> out(mf);
   {
@@ -882,7 +882,7 @@ std::vector<EP> dedup_device(Ctx& ctx, const CandSet& cs, const RefineDevOut& ro
     d2h(lab.data(), g_lab.get(), mf * stv, s);
     d2h(ie.data(), g_ie.get(), mf * stv, s);
     d2h(ed.data(), g_ed.get(), mf * stv, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
     for (uint32_t i = 0; i < mf; ++i) {
       EP& e = out[i];
       e.tx_id = tx[i];
@@ -1136,7 +1136,7 @@ void api_shard_trace(Ctx& ctx, const SceneDev& scene, const pcr_run_config& cfg,
       row += props[t].n;
     }
     st.n_rows = total;
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
   } catch (const std::exception& e) {
     stage_fail("trace", e);
   }
@@ -1201,12 +1201,12 @@ void api_shard_refine(Ctx& ctx, const SceneDev& scene, const void* rows, uint64_
       // iterations of this shard's candidates (a work counter, summed over shards)
       std::vector<uint32_t> all(n);
       d2h(all.data(), ro.iters.get(), n, s);
-      PCR_CUDA(cudaStreamSynchronize(s));
+      stream_wait(s);
       uint64_t sum = 0;
       for (uint32_t i = 0; i < n_sub; ++i) sum += all[st.shard + static_cast<size_t>(i) * st.n_shards];
       st.stats.refine_iterations = sum;
     }
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
   } catch (const std::exception& e) {
     stage_fail("refine", e);
   }
@@ -1274,7 +1274,7 @@ void api_shard_finish(Ctx& ctx, const void* rows, uint64_t n_rows, const pcr_sha
     }
     int h_bad = 0;
     d2h(&h_bad, bad.get(), 1, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
     if (h_bad) throw Error(PCR_ERR_INVALID, "shard: outcome rows do not cover the candidate list");
   } catch (const std::exception& e) {
     stage_fail("refine", e);

@@ -79,7 +79,7 @@ extern "C" int pcr_libm_exp_batch(pcr_ctx* ctx, const double* x, double* y, uint
       PCR_LAUNCH_CHECK();
     }
     pcr::d2h(y, dy.get(), n, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    pcr::stream_wait(s);
     return PCR_OK;
   } catch (const std::exception& e) {
     ctx->c.last_error = e.what();

@@ -1613,7 +1613,7 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     d2h(&h, nonuni.get(), 1, s);
     double r0 = 0.0;
     if (grid.n_ies) d2h(&r0, &grid.sc.get()->w, 1, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
     gv.ie_rr = rr.get();
     gv.rr_uniform = grid.n_ies && !h;
     gv.rr_radius = r0;
@@ -1647,7 +1647,7 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     exclusive_scan_u32(cnt.get(), nb_off.get(), nc, nb_off.get() + nc, s);
     uint32_t total = 0;
     d2h(&total, nb_off.get() + nc, 1, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
     nb_rec.alloc(total ? total : 1, s);
     nb_lab.alloc(total ? total : 1, s);
     count_launch();
@@ -1710,7 +1710,7 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
       PCR_CUDA(cudaMemsetAsync(dbg.get(), 0, 24ull * grid_n * kRefineThreads, s));
       unsigned long long* p = dbg.get();
       PCR_CUDA(cudaMemcpyToSymbolAsync(g_refine_dbg, &p, sizeof(p), 0, cudaMemcpyHostToDevice, s));
-      PCR_CUDA(cudaStreamSynchronize(s));
+      stream_wait(s);
       t0 = static_cast<unsigned long long>(std::chrono::duration_cast<std::chrono::nanoseconds>(
           std::chrono::system_clock::now().time_since_epoch()).count());
     }
@@ -1722,7 +1722,7 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     if (trace) {
       std::vector<unsigned long long> h(3ull * grid_n * kRefineThreads);
       d2h(h.data(), dbg.get(), h.size(), s);
-      PCR_CUDA(cudaStreamSynchronize(s));
+      stream_wait(s);
       unsigned long long* z = nullptr;
       PCR_CUDA(cudaMemcpyToSymbol(g_refine_dbg, &z, sizeof(z)));
       if (FILE* f = std::fopen(trace, "wb")) {
@@ -1737,7 +1737,7 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
       d2h(rs.data(), out.reason.get(), in.n, s);
       d2h(ni.data(), in.n_inter, in.n, s);
       d2h(kd.data(), in.kind, kd.size(), s);
-      PCR_CUDA(cudaStreamSynchronize(s));
+      stream_wait(s);
       if (FILE* f = std::fopen((std::string(trace) + ".cand").c_str(), "wb")) {
         for (uint32_t i = 0; i < in.n; ++i) {
           uint32_t kinds = 0;
@@ -1753,7 +1753,7 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
   PCR_LAUNCH_CHECK();
   unsigned long long hs[4];
   d2h(hs, stats.get(), 4, s);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   out.trials = hs[0];
   out.marches = hs[1];
   out.trial_nodes = hs[2];
@@ -1800,7 +1800,7 @@ void api_refine_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, cons
   d2h(len.data(), ro.length.get(), n, s);
   d2h(del.data(), ro.delay.get(), n, s);
   d2h(gn.data(), ro.gnorm.get(), n, s);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   pcr_paths& P = o->paths;
   for (size_t i = 0; i < n; ++i) {
     if (!o->has_path[i]) continue;

@@ -81,11 +81,15 @@ __device__ __forceinline__ bool make_ray(const Node& nd, uint32_t node_idx, uint
 
 __global__ void materialize_kernel(const Node* __restrict__ nodes, uint32_t node_begin,
                                    const uint64_t* __restrict__ prefix, uint32_t n_range, uint64_t v_begin,
-                                   uint32_t n_rays, GridView g, SceneView s, TraceCfg c, FanTable fan,
-                                   Ray* __restrict__ rays) {
+                                   uint32_t n_rays, const uint64_t* __restrict__ v_total, GridView g, SceneView s,
+                                   TraceCfg c, FanTable fan, Ray* __restrict__ rays) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n_rays) return;
   const uint64_t vk = v_begin + k;
+  if (vk >= *v_total) {  // past the range's last child ray (the host sizes chunks before it knows the total)
+    rays[k].alive = 0;
+    return;
+  }
   uint32_t lo = 0, hi = n_range;  // upper_bound(prefix, vk) - 1
   while (lo < hi) {
     const uint32_t m = (lo + hi) >> 1;
@@ -787,7 +791,7 @@ void transmission_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, u
   }
   uint32_t h_tot[2];
   d2h(h_tot, tot.get(), 2, s);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   out.n_los = h_tot[0];
   out.n_hits = h_tot[1];
   out.los_ie.alloc(out.n_los + 1, s);
@@ -811,7 +815,9 @@ namespace {
 struct StackEntry {
   uint32_t node_begin, n_nodes;
   DBuf<uint64_t> prefix;
+  DBuf<uint64_t> total;  // child rays of the range (device; read with the chunk's counters)
   uint64_t v_total, v_done;
+  bool known;            // v_total read back yet
 };
 
 __global__ void count_alive_kernel(const Ray* __restrict__ rays, uint32_t n, unsigned long long* __restrict__ c) {
@@ -883,7 +889,7 @@ static void kappa_select(Ctx& ctx, const GridDev& grid, const DBuf<Cand>& cands,
   int coll = 0;
   d2h(&coll, collision.get(), 1, s);
   d2h(&n_out, tot.get(), 1, s);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   if (coll) throw Error(4, "trace: group hash collision in kappa selection");
   DBuf<Cand> o(n_out ? n_out : 1, s);
   count_launch();
@@ -964,30 +970,33 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
     count_launch();
     children_kernel<<<nb(count), kT, 0, s>>>(nodes.get(), begin, count, cnt.get());
     PCR_LAUNCH_CHECK();
-    DBuf<uint64_t> tot(1, s);
-    exclusive_scan_u64(cnt.get(), e.prefix.get(), count, tot.get(), s);
-    d2h(&e.v_total, tot.get(), 1, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    e.total.alloc(1, s);
+    exclusive_scan_u64(cnt.get(), e.prefix.get(), count, e.total.get(), s);
+    // the total is read with the next chunk's counters (no round trip here): until then
+    // chunks are sized at the chunk bound and materialize clamps on the device total
+    e.v_total = 0;
+    e.known = false;
     e.v_done = 0;
-    if (e.v_total) stack.push_back(std::move(e));
+    stack.push_back(std::move(e));
   };
   push_range(0, n_local);
 
   while (!stack.empty()) {
     StackEntry& top = stack.back();
-    if (top.v_done >= top.v_total) {
+    if (top.known && top.v_done >= top.v_total) {
       stack.pop_back();
       continue;
     }
-    const uint32_t nr = static_cast<uint32_t>(std::min<uint64_t>(chunk, top.v_total - top.v_done));
+    const uint32_t nr =
+        static_cast<uint32_t>(top.known ? std::min<uint64_t>(chunk, top.v_total - top.v_done) : chunk);
     count_launch();
     {
       KTimer kt(ctx, "materialize");
       materialize_kernel<<<nb(nr), kT, 0, s>>>(nodes.get(), top.node_begin, top.prefix.get(), top.n_nodes,
-                                               top.v_done, nr, gv, sv, c, fan, rays.get());
+                                               top.v_done, nr, top.total.get(), gv, sv, c, fan, rays.get());
     }
     PCR_LAUNCH_CHECK();
-    top.v_done += nr;
+    const bool was_known = top.known;
     PCR_CUDA(cudaMemsetAsync(alive.get(), 0, sizeof(unsigned long long), s));
     count_launch();
     count_alive_kernel<<<nb(nr), kT, 0, s>>>(rays.get(), nr, alive.get());
@@ -1029,7 +1038,9 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
       PCR_LAUNCH_CHECK();
       d2h(h_cnt, counters.get(), 3, s);
       d2h(&h_alive, alive.get(), 1, s);
-      PCR_CUDA(cudaStreamSynchronize(s));
+      if (!top.known) d2h(&top.v_total, top.total.get(), 1, s);
+      stream_wait(s);
+      top.known = true;
       n_tasks = h_cnt[0];
       if (n_tasks <= task_cap) {
         n_nodes = h_cnt[1];
@@ -1039,6 +1050,7 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
       task_cap = static_cast<size_t>(n_tasks) * 5 / 4 + 1024;  // visibility did nothing: rerun the chunk
       tasks.alloc(task_cap, s);
     }
+    top.v_done += was_known ? nr : std::min<uint64_t>(nr, top.v_total);
     stats.cone_traces += h_alive;
     stats.visibility_tests += n_tasks;
     if (n_tasks == 0) continue;
@@ -1093,7 +1105,7 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
   unsigned long long ws[2] = {0, 0}, unresolved = 0;
   d2h(ws, walk_stats.get(), 2, s);
   PCR_CUDA(cudaMemcpyFromSymbolAsync(&unresolved, g_libm_unresolved, sizeof(unresolved), 0, cudaMemcpyDeviceToHost, s));
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   stats.walk_cells += ws[0];
   stats.walk_ies += ws[1];
   stats.libm_unresolved += unresolved;
@@ -1307,7 +1319,7 @@ void kappa_merge_rows(Ctx& ctx, const uint8_t* rows, uint64_t n64, uint32_t stri
   d2h(&coll, collision.get(), 1, s);
   d2h(&n_out, tot.get(), 1, s);
   if (n_tx) d2h(per_tx.data(), cnt.get(), n_tx, s);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   if (coll) throw Error(4, "trace: group hash collision in kappa selection");
   out.n = n_out;
 }
@@ -1330,7 +1342,7 @@ static void fill_paths_from_cands(const CandDev& cd, uint32_t tx_id, const doubl
   d2h(len.data(), cd.length.get(), n, s);
   d2h(pos.data(), cd.pos.get(), pos.size(), s);
   d2h(nrm.data(), cd.nrm.get(), nrm.size(), s);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   for (size_t k = 0; k < n; ++k) {
     const size_t r = row0 + k;
     p->tx_id[r] = tx_id;
@@ -1376,7 +1388,7 @@ void api_transmission(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
   std::vector<uint32_t> rxid(grid.n_ies);
   d2h(rp.data(), grid.rp.get(), grid.n_ies, s);
   d2h(rxid.data(), grid.rx.get(), grid.n_ies, s);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   pcr_paths* los = alloc_paths(t.n_los, 1);
   const double* txp = &scene.h_tx[3ull * tx_index];
   for (uint32_t k = 0; k < t.n_los; ++k) {
@@ -1453,7 +1465,7 @@ void api_cone_trace_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, 
       PCR_LAUNCH_CHECK();
     }
     d2h(&nt, cnt.get(), 1, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
     if (nt <= cap) break;
     cap = nt + 1024;
     tasks.alloc(cap, s);
@@ -1492,7 +1504,7 @@ void api_cone_trace_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, 
     PCR_LAUNCH_CHECK();
     std::vector<uint32_t> hc(n_rays);
     d2h(hc.data(), ecnt.get(), n_rays, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
     for (size_t k = 0; k < n_rays; ++k) eoff[k + 1] = eoff[k] + hc[k];
     DBuf<uint64_t> doff(n_rays + 1, s);
     h2d(doff.get(), eoff.data(), n_rays + 1, s);
@@ -1515,7 +1527,7 @@ void api_cone_trace_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, 
     PCR_LAUNCH_CHECK();
     std::vector<uint32_t> hc(n_rays);
     d2h(hc.data(), vcnt.get(), n_rays, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
     for (size_t k = 0; k < n_rays; ++k) voff[k + 1] = voff[k] + hc[k];
     DBuf<uint64_t> doff(n_rays + 1, s);
     h2d(doff.get(), voff.data(), n_rays + 1, s);
@@ -1527,7 +1539,7 @@ void api_cone_trace_batch(Ctx& ctx, const GridDev& grid, const SceneDev& scene, 
     vv.resize(voff[n_rays]);
     d2h(vv.data(), dvv.get(), vv.size(), s);
   }
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   // group by ray, ascending ie (tracer.cpp:400-401)
   std::vector<uint32_t> order;
   order.reserve(nt);
@@ -1597,7 +1609,7 @@ void api_segment_visible_batch(Ctx& ctx, const GridDev& grid, const SceneDev& sc
                                                                        scene.view(), vis.get());
   PCR_LAUNCH_CHECK();
   d2h(visible_out, vis.get(), n, s);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
 }
 
 }  // namespace pcr

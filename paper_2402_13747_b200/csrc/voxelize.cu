@@ -644,7 +644,7 @@ GridView GridDev::view_for(Ctx& ctx, const SceneDev& scene) const {
     }
     int h = 0;
     d2h(&h, f.get(), 1, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
     has_nonplanar = h;
   }
 #ifndef PCR_STAGE_PAYLOAD
@@ -676,7 +676,7 @@ void compute_march_distances_device(Ctx& ctx, GridDev& grid) {
   PCR_LAUNCH_CHECK();
   int any = 0;
   d2h(&any, flag.get(), 1, s);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
   if (!any) {
     count_launch();
     fill_march_kernel<<<blocks_for(n, kThreads), kThreads, 0, s>>>(grid.cells.get(), n, kMarchNoIes);
@@ -722,7 +722,7 @@ void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int d
     PCR_LAUNCH_CHECK();
     std::vector<BoundsPartial> hp(nb);
     d2h(hp.data(), part.get(), nb, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
     for (const auto& p : hp) {
       for (int a = 0; a < 3; ++a) {
         mn[a] = smin(mn[a], p.mn[a]);
@@ -803,7 +803,7 @@ void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int d
       exclusive_scan_u32(hist.get(), pre.get(), n_cells, tot.get(), s);
       std::vector<uint32_t> hp(n_cells);
       d2h(hp.data(), pre.get(), n_cells, s);
-      PCR_CUDA(cudaStreamSynchronize(s));
+      stream_wait(s);
       auto split = [&](uint32_t r) -> uint32_t {  // first voxel whose prefix reaches r N / n
         if (r == 0) return 0;
         if (r >= shard->n_shards) return static_cast<uint32_t>(n_cells);
@@ -821,7 +821,7 @@ void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int d
       PCR_LAUNCH_CHECK();
       exclusive_scan_u32(flag.get(), fpos.get(), N, cnt.get(), s);
       d2h(&n_in, cnt.get(), 1, s);
-      PCR_CUDA(cudaStreamSynchronize(s));
+      stream_wait(s);
     }
     shard_ids.alloc(n_in ? n_in : 1, s);
     if (n_in) {
@@ -873,7 +873,7 @@ void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int d
     PCR_LAUNCH_CHECK();
     exclusive_scan_u32(head.get(), ie_id.get(), N, n_surf_dev.get(), s);
     d2h(&n_surf, n_surf_dev.get(), 1, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
   }
   key.release();
 
@@ -912,7 +912,7 @@ void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int d
     DBuf<uint32_t> tot(1, s);
     exclusive_scan_u32(cnt.get(), piece_off.get(), n_edges, tot.get(), s);
     d2h(&n_pieces, tot.get(), 1, s);
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
   }
   uint32_t n_extra = n_pieces + n_rx;
   DBuf<ExtraIE> extra(n_extra ? n_extra : 1, s), extra_sorted(n_extra ? n_extra : 1, s);
@@ -937,7 +937,7 @@ void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int d
     if (shard) {  // the shard keeps the edge pieces and receivers of its voxel range (few)
       std::vector<ExtraIE> h(n_extra), k;
       d2h(h.data(), extra_sorted.get(), n_extra, s);
-      PCR_CUDA(cudaStreamSynchronize(s));
+      stream_wait(s);
       for (const ExtraIE& x : h)
         if (x.voxel >= v_lo && x.voxel < v_hi) k.push_back(x);
       n_extra = static_cast<uint32_t>(k.size());
@@ -975,7 +975,7 @@ void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int d
   }
   if (shard) {  // a part: cells and march distances come with the assembled grid
     out.cells.release();
-    PCR_CUDA(cudaStreamSynchronize(s));
+    stream_wait(s);
     return;
   }
   if (n_ies) {
@@ -986,7 +986,7 @@ void build_grid_device(Ctx& ctx, const SceneDev& scene, double voxel_size, int d
   }
   // ---- K9
   compute_march_distances_device(ctx, out);
-  PCR_CUDA(cudaStreamSynchronize(s));
+  stream_wait(s);
 }
 
 }  // namespace pcr
