@@ -699,6 +699,7 @@ struct ScanSlot {  // one per lane: the reprojection it posted and its best reco
 // iterations mostly reproject into the same cell, so the two binary searches are skipped.
 struct RunCache {
   uint32_t cell, label, j0, len;
+  uint32_t win;  // the last scan's winner, as a position in this run (kNoRec: none)
 };
 
 template <int D>
@@ -963,7 +964,7 @@ __device__ __forceinline__ int reproject_setup(const V3& prev, const V3& predict
     if (g.nb_lab[m] <= label) lo = m + 1; else hi = m;
   }
   len = lo - j0;
-  rc = RunCache{c, label, j0, len};
+  rc = RunCache{c, label, j0, len, 0xffffffffu};
   return 1;
 }
 
@@ -1014,6 +1015,8 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
 #define PCR_FAST_REJECT 0
 #endif
   const bool fast = PCR_FAST_REJECT && g.fast_reject != 0;
+  const bool uniform = g.rr_uniform != 0;
+  const double uradius = g.rr_radius;
   long long c_num = cache->c_num, c_dn = cache->c_dn;
   double c_t = cache->c_t;
   uint32_t n_march = cache->n_march;
@@ -1025,9 +1028,12 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
   const uint32_t total = __shfl_sync(kFull, incl, 31);
   const uint32_t pre = incl - len;
   ScanSlot& me = ws[lane];
-  me.best_f = kNoRec;
+  // the caller may seed the best with its last winner (best_f = position in the run):
+  // the scan then only evaluates records that can still beat it, (t, index)-wise
+  const uint32_t seed = len ? me.best_f : kNoRec;
+  me.best_f = seed == kNoRec ? kNoRec : pre + seed;
   if (total == 0) return;
-  me.best_t = 1.7976931348623157e308;
+  if (seed == kNoRec) me.best_t = 1.7976931348623157e308;
   me.pre = pre;
   __syncwarp();
   const double radius = 2.0 * g.sub_edge;
@@ -1046,23 +1052,29 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
     if (valid) {
       const ScanSlot& sl = ws[o];
       const uint32_t j = sl.j0 + (F - sl.pre);
-      // the record and its plane side by side (no dependent load through the IE index)
+      // the record first; its plane (side arrays, no dependent load through the IE
+      // index) only for records that survive the radius and window tests
       const double4 r4 = ldg4(nb_rec + j);
-      const double4 pa = ldg4(nb_pa + j);
-      const double4 pb = ldg4(nb_pb + j);
       const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r4.w));
       const uint32_t ie = static_cast<uint32_t>(w >> 33);
       const V3 sc = ld3(r4);
-      const double rad = pa.w;
+      const double rad = uniform ? uradius : __ldg(&nb_pa[j].w);
       const V3 pq{sl.pred[0], sl.pred[1], sl.pred[2]};
       if (norm_le(sc - pq, radius + rad)) {
         ++n_march;  // counts the reference's march_segment call
         const V3 pv{sl.prev[0], sl.prev[1], sl.prev[2]}, dv{sl.dir[0], sl.dir[1], sl.dir[2]};
         const double t_center = dot(sc - pv, dv);
         const double t_lo = smax(0.0, t_center - rad);
-        double bt = sl.best_t;
-        if (t_lo < bt) {
+        const double best = sl.best_t;
+        // every hit of this window lies at t >= t_lo: it can only win if t_lo < best,
+        // or t_lo == best with a lower record index than the best's (seeds may sit
+        // anywhere in the run); a lower index wins ties, so its bound admits t == best
+        const bool lower = F < sl.best_f;
+        if (t_lo < best || (t_lo == best && lower)) {
+          double bt = lower ? nextafter(best, inf) : best;
           if (__builtin_expect(((w >> 32) & 1u) != 0, 1)) {  // planar records are the common case
+            const double4 pa = ldg4(nb_pa + j);
+            const double4 pb = ldg4(nb_pb + j);
             if (planar_candidate_at(pv, dv, ld3(pa), ld3(pb), eps, t_lo, t_center + rad, bt, c_num, c_dn, c_t, fast))
               t = bt;
           } else {
@@ -1099,7 +1111,7 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
       }
     }
     __syncwarp();
-    if (valid && ((heads >> lane) & 1u) && bt < ws[o].best_t) {
+    if (valid && ((heads >> lane) & 1u) && (bt < ws[o].best_t || (bt == ws[o].best_t && bf < ws[o].best_f))) {
       ws[o].best_t = bt;
       ws[o].best_f = bf;
     }
@@ -1109,6 +1121,40 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
   cache->c_dn = c_dn;
   cache->c_t = c_t;
   cache->n_march = n_march;
+}
+
+// The seed of a same-label scan: the record at position `win` of the run (the node's
+// previous winner), evaluated exactly as the scan evaluates a record against an empty
+// best — radius test, window, planar snap or march. A hit becomes the scan's initial
+// best (t, position); a miss leaves the scan unseeded. Not counted in n_march (the scan
+// visits and counts the record itself).
+#ifndef PCR_SCAN_SEED
+#define PCR_SCAN_SEED 1
+#endif
+__device__ __noinline__ void seed_winner(const V3& prev, const V3& dir, const V3& pred, uint32_t j0, uint32_t win,
+                                         const GridView& g, const SceneView& s, ScanSlot& me) {
+  const uint32_t j = j0 + win;
+  const double4 r4 = ldg4(g.nb_rec + j);
+  const double4 pa = ldg4(g.nb_pa + j);
+  const V3 sc = ld3(r4);
+  const double rad = pa.w;
+  if (!norm_le(sc - pred, 2.0 * g.sub_edge + rad)) return;
+  const double t_center = dot(sc - prev, dir);
+  const double t_lo = smax(0.0, t_center - rad);
+  const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r4.w));
+  double bt = 1.7976931348623157e308;
+  if ((w >> 32) & 1u) {
+    const double4 pb = ldg4(g.nb_pb + j);
+    long long c_num = 0x7ff8dead7ff8deadll, c_dn = 0x7ff8dead7ff8deadll;
+    double c_t = 0.0;
+    if (!planar_candidate_at(prev, dir, ld3(pa), ld3(pb), g.hit_eps, t_lo, t_center + rad, bt, c_num, c_dn, c_t))
+      return;
+  } else {
+    bt = march_np(prev.x, prev.y, prev.z, dir.x, dir.y, dir.z, static_cast<uint32_t>(w >> 33), g, s, bt);
+    if (!(bt < __longlong_as_double(0x7ff0000000000000ll))) return;
+  }
+  me.best_t = bt;
+  me.best_f = win;
 }
 
 // Prefetching variant of the packed scan (PCR_SCAN_PREFETCH=1; measured slower and off:
@@ -1407,6 +1453,11 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
           me.dir[0] = dir.x, me.dir[1] = dir.y, me.dir[2] = dir.z;
           me.pred[0] = pred.x, me.pred[1] = pred.y, me.pred[2] = pred.z;
           me.j0 = j0;
+          // seed the scan with this node's last winner when it still hits: the scan
+          // then evaluates only the records that could beat it (coop_scan)
+          me.best_f = kNoRec;
+          me.best_t = 1.7976931348623157e308;
+          if (PCR_SCAN_SEED && st.rc[q].win < len) seed_winner(prev, dir, pred, j0, st.rc[q].win, g, s, me);
         } else if (r == 2) {
           got = reproject(prev, pred, st.nd[q].label, g, s, re, n_march);
         }
@@ -1422,6 +1473,7 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
         const V3 prev{me.prev[0], me.prev[1], me.prev[2]}, dir{me.dir[0], me.dir[1], me.dir[2]};
         const V3 pred{me.pred[0], me.pred[1], me.pred[2]};
         const uint32_t bf = len ? me.best_f : kNoRec;
+        st.rc[q].win = bf != kNoRec ? bf - me.pre : kNoRec;
         if (bf != kNoRec) {
           const double bt = me.best_t;
           const uint32_t ie =
