@@ -1,5 +1,5 @@
 """Every BASELINE.json config on one B200, beside the reference on
-the host cores. Writes one JSON document (default profiles/configs_r01.json).
+the host cores. Writes one JSON document (default profiles/configs_r02.json).
 
   C1-C4  full pipeline (run_pipeline_device, scene resident): step seconds, launched
          Mrays/s, exact paths/s, candidates refined/s, stage and kernel split. The CPU
@@ -46,7 +46,7 @@ def gpu_pipeline(name, reps, mi=None):
     ds = pcray.DeviceScene(scene, ctx)
     conf = abi.default_run_config(**run)
     stream = torch.cuda.ExternalStream(pcray.stream_ptr(ctx))
-    big = name in ("C3", "C4")
+    big = name in ("C2", "C3", "C4", "C2np")
     if not big:
         pcray.run_pipeline_device(ds, conf)  # warm-up (first-call allocations; noise next to C3/C4 steps)
     ms, s = [], None
@@ -190,14 +190,14 @@ def ply_ingest(points, cpu):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="C1,C2,C2np,C3,C4")
+    ap.add_argument("--configs", default="C1,C2d3,C2,C3")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--c5", action="store_true")
     ap.add_argument("--ply", type=int, default=0, help="PLY ingest benchmark with this many points")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--cpu-c5-max", type=int, default=10_000_000)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "configs_r01.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "configs_r02.json"))
     args = ap.parse_args()
     doc = {"device": None, "pipelines": [], "c5": None}
     try:
@@ -211,7 +211,7 @@ def main():
         print(json.dumps(row), flush=True)
         if not args.no_cpu:
             try:
-                row["cpu"] = cpu_pipeline(scene, run, args.cpu_budget, probe=64 if name in ("C1", "C2") else 4096)
+                row["cpu"] = cpu_pipeline(scene, run, args.cpu_budget, probe=64 if name in ("C1", "C2", "C2d3") else 4096)
             except Exception as e:
                 row["cpu"] = {"kind": "reference", "error": str(e)}
             print(json.dumps(row["cpu"]), flush=True)
