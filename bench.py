@@ -272,10 +272,15 @@ def b200_arm(args, rank, world, local_rank):
 
     for _ in range(args.warmup):
         step()
+    # kernel shares from one profiled step outside the timed region (events around every
+    # launch would add host work to the timed steps)
+    _, _, _, _, kshares = timed_steps(step, 1, profile=1)
     barrier()
     with ClockSampler(dev) as clocks:
         barrier()
-        ms, outs, launches, _, ktimes = timed_steps(step, args.steps, profile=True)
+        # timed steps: events only around the refine launch (the roofline's kernel, one
+        # launch per step) — its average duration over the timed region
+        ms, outs, launches, _, ktimes = timed_steps(step, args.steps, profile=2)
         barrier()
     step_ms = max_over_ranks(sum(ms)) / args.steps
     launches = int(sum_over_ranks(launches))
@@ -321,8 +326,8 @@ def b200_arm(args, rank, world, local_rank):
     fp64 = pcray.fp64_probe(ctx)
     dom = max(ktimes.items(), key=lambda kv: kv[1][0]) if ktimes else ("none", (0.0, 1))
     rl = roofline(dom[0], dom[1][0] / args.steps, max(1, dom[1][1] // args.steps), own, peaks, peaks_kind, fp64)
-    total_k = sum(v[0] for v in ktimes.values())
-    shares = {k: round(v[0] / total_k, 4) for k, v in sorted(ktimes.items(), key=lambda kv: -kv[1][0])}
+    total_k = sum(v[0] for v in kshares.values())
+    shares = {k: round(v[0] / total_k, 4) for k, v in sorted(kshares.items(), key=lambda kv: -kv[1][0])}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

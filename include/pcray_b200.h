@@ -454,7 +454,9 @@ int pcr_shard_finish(pcr_ctx* ctx, const void* outcome_rows_device, uint64_t n_r
 /* ---- instrumentation (no reference counterpart) ------------------------------------ */
 /* cudaStream_t the context launches on, as an opaque pointer (for caller-side events) */
 void* pcr_stream(pcr_ctx* ctx);
-/* per-kernel CUDA-event timing of subsequent calls: on != 0 enables, 0 disables */
+/* per-kernel CUDA-event timing of subsequent calls: 1 every kernel, 2 only the refine
+ * kernel (one launch per refine call: no events around the many small trace launches
+ * inside a timed region), 0 disables */
 int pcr_set_profiling(pcr_ctx* ctx, int on);
 /* accumulated per-kernel totals since the last reset; returns the number of entries
  * (at most cap); names are NUL-terminated, 32 bytes each. reset != 0 clears them. */

@@ -507,7 +507,7 @@ void* pcr_stream(pcr_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c.stream) 
 int pcr_set_profiling(pcr_ctx* ctx, int on) {
   return guarded(ctx, [&] {
     ctx->c.resolve_timers();
-    ctx->c.profiling = on != 0;
+    ctx->c.profiling = on == 2 ? 2 : on != 0 ? 1 : 0;
   });
 }
 

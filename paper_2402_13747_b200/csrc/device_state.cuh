@@ -5,6 +5,7 @@
 
 #include <array>
 #include <atomic>
+#include <cstring>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -148,7 +149,7 @@ struct Ctx {
   // work counters of the last pcr_propagate call (cone traces, visibility tests, cells, IEs)
   uint64_t last_trace[5] = {0, 0, 0, 0, 0};
   // per-kernel CUDA-event timing (pcr_set_profiling); resolved lazily
-  bool profiling = false;
+  int profiling = 0;  // 0 off, 1 every kernel, 2 only the refine kernel (one launch per call)
   struct Pending {
     const char* name;
     cudaEvent_t a, b;
@@ -170,13 +171,15 @@ struct KTimer {
   cudaEvent_t a = nullptr, b = nullptr;
   double units;
   KTimer(Ctx& ctx, const char* n, double u = 0) : c(ctx), name(n), units(u) {
-    if (!c.profiling) return;
+    if (c.profiling == 2 && std::strcmp(n, "refine") != 0) c_skip = true;
+    if (!c.profiling || c_skip) return;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a, c.stream);
   }
+  bool c_skip = false;
   ~KTimer() {
-    if (!c.profiling) return;
+    if (!c.profiling || c_skip) return;
     cudaEventRecord(b, c.stream);
     c.pending.push_back({name, a, b, units});
   }
