@@ -1744,10 +1744,16 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
                 : in.stride <= 5                    ? refine_warp_kernel<5, kWarpMinBlocks>
                                                     : refine_warp_kernel<kMaxDepth, kWarpMinBlocks>;
     auto kern2 = in.stride <= 3 ? refine_kernel<3, 4> : in.stride <= 5 ? refine_kernel<5, 4> : refine_kernel<kMaxDepth, 4>;
-#ifdef PCR_REFINE_CARVEOUT
-    if (warp)
-      PCR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, PCR_REFINE_CARVEOUT));
+    // shared-memory carveout: the kernel needs 3 x 13.4 KB (scan slots), and the driver's
+    // own choice for it was the 100 KB configuration (ncu launch__shared_mem_config_size
+    // 102.4 KB), leaving L1 short for the per-lane path state. A 25 % hint selects the
+    // 64 KB configuration: C2d3 refine 620 -> 608 ms, C2 7.60 -> 7.43 s (same box,
+    // profiles/ab_carveout_r02.log); 0 % starves occupancy (1.10 s), 60 % is slower.
+#ifndef PCR_REFINE_CARVEOUT
+#define PCR_REFINE_CARVEOUT 25
 #endif
+    if (warp && PCR_REFINE_CARVEOUT >= 0)
+      PCR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, PCR_REFINE_CARVEOUT));
     if (warp)
       PCR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRefineThreads, 0));
     else
