@@ -1123,6 +1123,171 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
   cache->n_march = n_march;
 }
 
+// Two-records-per-lane variant of the packed scan (PCR_SCAN_ILP2=1): rounds of 64
+// records, lane l evaluating positions base + l and base + 32 + l with straight-line
+// code (both records' loads, radius tests, windows, plane snaps and endpoint tests
+// computed unconditionally and combined by selects), so each lane carries two
+// independent FP64 chains through the round instead of one. Same decisions per record
+// as planar_candidate_at (the division cache is not used: t* is recomputed, same
+// bits); non-planar records march afterwards. The second half prunes against the
+// bests from before the first half's update, which only evaluates more records. The
+// two halves are then reduced and merged into the owners' bests one after the other.
+#ifndef PCR_SCAN_ILP2
+#define PCR_SCAN_ILP2 0
+#endif
+__shared__ uint8_t g_owner_at2[2 * kRefineThreads];
+
+__device__ PCR_COOP_INLINE void coop_scan_ilp2(int lane, uint32_t len, const GridView& g, const SceneView& s,
+                                               ScanCache* cache) {
+  const uint32_t wb = threadIdx.x & ~31u;
+  ScanSlot* ws = g_slots + wb;
+  uint8_t* owner_at = g_owner_at2 + 2 * wb;
+  const double4* __restrict__ nb_rec = g.nb_rec;
+  const double4* __restrict__ nb_pa = g.nb_pa;
+  const double4* __restrict__ nb_pb = g.nb_pb;
+  const double eps = g.hit_eps;
+  const bool uniform = g.rr_uniform != 0;
+  const double uradius = g.rr_radius;
+  uint32_t n_march = cache->n_march;
+  uint32_t incl = len;
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t v = __shfl_up_sync(kFull, incl, off);
+    if (lane >= off) incl += v;
+  }
+  const uint32_t total = __shfl_sync(kFull, incl, 31);
+  const uint32_t pre = incl - len;
+  ScanSlot& me = ws[lane];
+  const uint32_t seed = len ? me.best_f : kNoRec;
+  me.best_f = seed == kNoRec ? kNoRec : pre + seed;
+  if (total == 0) return;
+  if (seed == kNoRec) me.best_t = 1.7976931348623157e308;
+  me.pre = pre;
+  __syncwarp();
+  const double radius = 2.0 * g.sub_edge;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  const uint32_t lmask = kFull >> (31 - lane);  // lanes 0..lane
+  int carry = 0;
+  for (uint32_t base = 0; base < total; base += 64) {
+    const uint32_t rel = pre - base;
+    const bool in_round = len && pre >= base && rel < 64u;
+    if (in_round) owner_at[rel] = static_cast<uint8_t>(lane);
+    const uint32_t sm0 = __reduce_or_sync(kFull, in_round && rel < 32u ? 1u << rel : 0u);
+    const uint32_t sm1 = __reduce_or_sync(kFull, in_round && rel >= 32u ? 1u << (rel - 32u) : 0u);
+    __syncwarp();
+    const uint32_t b0 = sm0 & lmask, b1 = sm1 & lmask;
+    const int last0 = sm0 ? owner_at[31 - __clz(sm0)] : carry;  // owner of position base + 31
+    int o[2];
+    o[0] = b0 ? owner_at[31 - __clz(b0)] : carry;
+    o[1] = b1 ? owner_at[63 - __clz(b1)] : last0;
+    uint32_t F[2] = {base + lane, base + 32 + lane};
+    bool valid[2] = {F[0] < total, F[1] < total};
+    double t[2];
+    bool np[2];
+    double4 r4[2], pa[2], pb[2];
+    uint32_t j[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const ScanSlot& sl = ws[valid[k] ? o[k] : 0];
+      j[k] = valid[k] ? sl.j0 + (F[k] - sl.pre) : 0u;
+      r4[k] = ldg4(nb_rec + j[k]);
+      pa[k] = ldg4(nb_pa + j[k]);
+      pb[k] = ldg4(nb_pb + j[k]);
+    }
+    bool band[2], near[2], cand[2];
+    double bt[2], yv[2], sq[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const ScanSlot& sl = ws[valid[k] ? o[k] : 0];
+      const V3 sc = ld3(r4[k]);
+      const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r4[k].w));
+      const bool planar = ((w >> 32) & 1u) != 0;
+      const double rad = uniform ? uradius : pa[k].w;
+      const V3 pq{sl.pred[0], sl.pred[1], sl.pred[2]};
+      const V3 pv{sl.prev[0], sl.prev[1], sl.prev[2]}, dv{sl.dir[0], sl.dir[1], sl.dir[2]};
+      // norm_le(sc - pq, radius + rad), its band resolved below
+      yv[k] = radius + rad;
+      sq[k] = sqnorm(sc - pq);
+      const double yy = yv[k] * yv[k];
+      const bool in_ = sq[k] <= yy * (1.0 - 1e-12), out_ = sq[k] >= yy * (1.0 + 1e-12);
+      band[k] = valid[k] && !in_ && !out_;
+      near[k] = in_;
+      const double t_center = dot(sc - pv, dv);
+      const double t_lo = smax(0.0, t_center - rad);
+      const double t_hi = t_center + rad;
+      const double best = sl.best_t;
+      const bool lower = F[k] < sl.best_f;
+      cand[k] = valid[k] && (t_lo < best || (t_lo == best && lower));
+      // nextafter(best, +inf) for best >= +0 (bests are hit distances >= 0 or DBL_MAX)
+      bt[k] = lower ? __longlong_as_double(__double_as_longlong(best) + 1) : best;
+      // planar_candidate_at without early exits (same operations, same bits)
+      const V3 pp = ld3(pa[k]), pn = ld3(pb[k]);
+      const double dn = dot(dv, pn);
+      const bool snap = fabs(dn) > 1e-12;
+      const double num = dot(pp - pv, pn);
+      const double t_star = num / dn;
+      const bool in_win = snap && t_star >= t_lo && t_star <= t_hi;
+      const double f = dot((pv + t_lo * dv) - pp, pn);
+      const double f_hi = dot((pv + t_hi * dv) - pp, pn);
+      const bool hit_lo = fabs(f) <= eps, sign = f * f_hi < 0.0, hit_hi = fabs(f_hi) <= eps;
+      const double tc = hit_lo ? t_lo : sign ? 0.5 * (t_lo + t_hi) : t_hi;
+      const double tt = in_win ? t_star : tc;
+      const bool hit = t_hi > t_lo && (hit_lo || sign || hit_hi) && tt < bt[k];
+      t[k] = planar && hit ? tt : inf;
+      np[k] = !planar;
+    }
+    if (__any_sync(kFull, band[0] || band[1])) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (band[k]) near[k] = sqrt(sq[k]) <= yv[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      n_march += valid[k] && near[k];  // counts the reference's march_segment call
+      if (!(valid[k] && near[k] && cand[k])) t[k] = inf;
+      np[k] = np[k] && valid[k] && near[k] && cand[k];
+    }
+    if (__any_sync(kFull, np[0] || np[1])) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (np[k]) {
+          const ScanSlot& sl = ws[o[k]];
+          const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r4[k].w));
+          t[k] = march_np(sl.prev[0], sl.prev[1], sl.prev[2], sl.dir[0], sl.dir[1], sl.dir[2],
+                          static_cast<uint32_t>(w >> 33), g, s, bt[k]);
+        }
+      }
+    }
+    carry = __shfl_sync(kFull, valid[1] ? o[1] : 32, 31);
+    // the two halves' segmented (t, F) mins, merged into the owners' bests in order
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (!__any_sync(kFull, t[k] < inf)) continue;
+      const uint32_t heads = (k == 0 ? sm0 : sm1) | 1u;
+      const uint32_t above = heads & ~lmask;
+      const int seg_end = above ? __ffs(above) - 1 : 32;
+      double bv = t[k];
+      uint32_t bf = F[k];
+      for (int off = 1; off < 32; off <<= 1) {
+        const double ot = __shfl_down_sync(kFull, bv, off);
+        const uint32_t of = __shfl_down_sync(kFull, bf, off);
+        if (lane + off < seg_end && ot < bv) {
+          bv = ot;
+          bf = of;
+        }
+      }
+      __syncwarp();
+      const int ok = o[k];
+      if (valid[k] && ((heads >> lane) & 1u) &&
+          (bv < ws[ok].best_t || (bv == ws[ok].best_t && bf < ws[ok].best_f))) {
+        ws[ok].best_t = bv;
+        ws[ok].best_f = bf;
+      }
+      __syncwarp();
+    }
+  }
+  cache->n_march = n_march;
+}
+
 // The seed of a same-label scan: the record at position `win` of the run (the node's
 // previous winner), evaluated exactly as the scan evaluates a record against an empty
 // best — radius test, window, planar snap or march. A hit becomes the scan's initial
@@ -1462,7 +1627,9 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
           got = reproject(prev, pred, st.nd[q].label, g, s, re, n_march);
         }
       }
-      if (PCR_SCAN_OWNER)
+      if (PCR_SCAN_ILP2)
+        coop_scan_ilp2(lane, coop ? len : 0u, g, s, &cache);
+      else if (PCR_SCAN_OWNER)
         coop_scan_owner(lane, coop ? len : 0u, g, s, &cache);
       else if (PCR_SCAN_PREFETCH)
         coop_scan_pf(lane, coop ? len : 0u, g, s, &cache);
