@@ -6,6 +6,8 @@ oracle finishes in seconds, plus size-independent properties at full size:
   two TXs bitwise, propagate on a deterministic sample of initial hits (the
   reference API takes the hit list, tracer.hpp:122) bitwise, and refine_path on the
   resulting candidates (reasons exact, geometry bitwise / within 1e-4 m).
+* C2-np (the office with tilted normals, every IE non-planar) the same way at its
+  contract depth 4 / 1: every march, projection and polish through the Gaussian SDF.
 * C5 (voxelization sweep): the grid bitwise at 1M and 3M points for several
   (voxel, D_v), and at 30M points the properties the reference's own tests state:
   point_indices is a permutation, IE ranges tile it, every point sits in its IE's
@@ -52,12 +54,14 @@ def test_config_grid(big, name):
     assert_grid_equal(dg.to_dict(), rg.to_dict())
 
 
-# initial-hit samples per TX at the contract depth (C3 3 / 0, C4 5 / 1): sized so the
-# oracle finishes in seconds; C4's sample includes edge hits (Keller fans, ~270 rays each)
-SAMPLES = {"C3": (6, 0), "C4": (8, 2)}
+# initial-hit samples per TX at the contract depth (C3 3 / 0, C4 5 / 1, C2-np 4 / 1):
+# sized so the oracle finishes in seconds; C4's and C2-np's samples include edge hits
+# (Keller fans, ~270 rays each). C2-np's candidates refine through the Gaussian SDF on
+# both sides (the oracle's refine is the slow part: ~100 candidates in ~10 s).
+SAMPLES = {"C3": (6, 0), "C4": (8, 2), "C2np": (4, 1)}
 
 
-@pytest.mark.parametrize("name", ["C3", "C4"])
+@pytest.mark.parametrize("name", ["C3", "C4", "C2np"])
 def test_config_trace_and_refine_sample(oracle, big, name):
     """transmission_phase bitwise for the first and last TX; propagate at the contract
     depth (no depth cap) on a deterministic initial-hit sample, per path bitwise, with
@@ -67,7 +71,7 @@ def test_config_trace_and_refine_sample(oracle, big, name):
     run = cfg.run
     n_tasks, n_edge = SAMPLES[name]
     tp = abi.trace_params(max_interactions=run["max_interactions"], max_diffractions=run["max_diffractions"])
-    for tx in [0, len(scene.tx) - 1]:
+    for tx in sorted({0, len(scene.tx) - 1}):
         ref_los, ref_hits = oracle.transmission_phase(rg, rs, tx, tp)
         los, hits = pcray.transmission_phase(tx, dg, ds, tp)
         assert_paths_equal(los, ref_los, ["tx_id", "rx_id", "tx_position", "rx_position", "length", "n_inter"])
