@@ -184,8 +184,33 @@ __device__ __forceinline__ ConeConsts cone_consts(double alpha, const V3& d) {
   k.fast = alpha >= 0.0 && alpha < 1.0 && k.dnorm > 0.0;
   return k;
 }
+#ifndef PCR_CONE_NODIV
+#define PCR_CONE_NODIV 1
+#endif
 __device__ __forceinline__ bool cone_test(const V3& o, const V3& d, const ConeConsts& k, const V3& c, double r) {
   const V3 vc = c - o;
+  if (PCR_CONE_NODIV) {
+    // The same decision with one square root and no division in the common case.
+    // dist <= r is norm_le (the squared norm outside its rounding band, sqrt inside).
+    // Multiplying cb >= cr by dist |d| > 0: P = vc.d against
+    // Q = |d| (cos(alpha) sqrt(dist^2 - r^2) - sin(alpha) r). P and Q carry ~1e-15
+    // dist |d| of rounding, so |P - Q| > T = 1e-9 |d| |vc|_1 (>= 1e-9 |d| dist) means
+    // |cb - cr| > 1e-9 in exact arithmetic, the fast path's certified margin above.
+    // dist^2 - r^2 is used only when it is >= 1e-6 dist^2 (its rounding then stays
+    // below 1e-10 relative, so the square root is well conditioned); grazing spheres
+    // and everything inside the margin take the reference's expression below.
+    if (norm_le(vc, r)) return true;
+    const double d2 = sqnorm(vc), q2 = d2 - r * r;
+    if (k.fast && q2 >= 1e-6 * d2) {
+      const double P = dot(vc, d);
+      const double Q = k.dnorm * (k.ca * sqrt(q2) - k.sa * r);
+      const double T = 1e-9 * k.dnorm * ((fabs(vc.x) + fabs(vc.y)) + fabs(vc.z));
+      if (P - Q > T) return true;
+      if (P - Q < -T) return false;
+    }
+    const double beta = angle_between(vc, d);
+    return libm_le(beta, k.alpha + asin(smin(1.0, r / norm(vc))), 8.0);
+  }
   const double dist = norm(vc);
   if (dist <= r) return true;
   if (k.fast) {
