@@ -770,7 +770,17 @@ __device__ PCR_STEP_INLINE bool path_init(PathState<D>& st, uint32_t k, const Ca
   return true;
 }
 
-// converged: final per-segment visibility (refine.cpp:256-265) and the refined path
+// converged: final per-segment visibility (refine.cpp:256-265) and the refined path.
+// The warp kernel defers the visibility part (PCR_DEFER_VIS, default): it writes the
+// refined path with the private reason kPendingVis, and converged_vis_kernel runs the
+// d + 1 segment tests afterwards with warp_segment_visible, 32 lanes per segment,
+// instead of one lane walking alone while its warp-mates wait (the converging lane is
+// alone in this branch). An occluded path then gets the outcome the inline test gives:
+// reason occluded, no path, the candidate's own points / normals / labels.
+#ifndef PCR_DEFER_VIS
+#define PCR_DEFER_VIS 1
+#endif
+constexpr int32_t kPendingVis = 0x7fff0001;
 template <int D>
 __device__ PCR_STEP_INLINE void path_converged(const PathState<D>& st, const CandIn& in, const GridView& g, const SceneView& s,
                                const RefOut& o) {
@@ -778,14 +788,16 @@ __device__ PCR_STEP_INLINE void path_converged(const PathState<D>& st, const Can
   const int d = st.d;
   V3 pts[D];
   for (int q = 0; q < d; ++q) pts[q] = node_point(st.nd[q], st.nd[q].p0, st.nd[q].p1);
-  V3 prev = st.tx;
-  for (int q = 0; q <= d; ++q) {
-    const V3 next = q < d ? pts[q] : st.rx;
-    if (!segment_visible(prev, next, kNoIe, g, s)) {
-      o.reason[k] = PCR_OCCLUDED;
-      return;
+  if (!PCR_DEFER_VIS) {
+    V3 prev = st.tx;
+    for (int q = 0; q <= d; ++q) {
+      const V3 next = q < d ? pts[q] : st.rx;
+      if (!segment_visible(prev, next, kNoIe, g, s)) {
+        o.reason[k] = PCR_OCCLUDED;
+        return;
+      }
+      prev = next;
     }
-    prev = next;
   }
   for (int q = 0; q < d; ++q) {
     const size_t j = static_cast<size_t>(k) * in.stride + q;
@@ -799,7 +811,7 @@ __device__ PCR_STEP_INLINE void path_converged(const PathState<D>& st, const Can
   o.length[k] = total;
   o.delay[k] = total / kSpeedOfLight;
   o.gnorm[k] = st.gnorm;
-  o.reason[k] = PCR_NOT_CONVERGED;
+  o.reason[k] = PCR_DEFER_VIS ? kPendingVis : PCR_NOT_CONVERGED;
   o.has_path[k] = 1;
 }
 
@@ -1785,6 +1797,48 @@ __global__ void nb_geo_kernel(GridView g, uint32_t total, const double4* __restr
   pb[j] = make_double4(pn.x, pn.y, pn.z, 0.0);
 }
 
+// The deferred final visibility of converged paths (path_converged): one warp per
+// pending candidate, segments tx -> p_0 -> ... -> p_{d-1} -> rx through
+// warp_segment_visible (the same predicate as segment_visible, tested bitwise by the
+// trace suites); any blocked segment makes the path occluded.
+__global__ void __launch_bounds__(128) converged_vis_kernel(const __grid_constant__ CandIn in, uint32_t n_sub,
+                                                            const __grid_constant__ GridView g,
+                                                            const __grid_constant__ SceneView s,
+                                                            const __grid_constant__ RefOut o) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n_sub; i += warps) {
+    const uint32_t k = in.first + i * in.step;
+    if (o.reason[k] != kPendingVis) continue;
+    const int d = static_cast<int>(in.n_inter[k]);
+    const V3 tx = load3(in.tx + 3ull * k), rx = load3(in.rx + 3ull * k);
+    bool visible = true;
+    V3 prev = tx;
+    for (int q = 0; q <= d && visible; ++q) {
+      const V3 next = q < d ? load3(o.pos + 3 * (static_cast<size_t>(k) * in.stride + q)) : rx;
+      visible = warp_segment_visible(prev, next, kNoIe, g, s);
+      prev = next;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (visible) {
+        o.reason[k] = PCR_NOT_CONVERGED;
+      } else {
+        o.reason[k] = PCR_OCCLUDED;
+        o.has_path[k] = 0;
+        for (int q = 0; q < d; ++q) {
+          const size_t j = static_cast<size_t>(k) * in.stride + q;
+          store3(o.pos + 3 * j, load3(in.pos + 3 * j));
+          if (in.kind[j] == 0) {
+            store3(o.nrm + 3 * j, load3(in.nrm + 3 * j));
+            o.label[j] = in.label[j];
+          }
+        }
+      }
+    }
+  }
+}
+
 // Visiting order of the warp kernel: candidates stably sorted by (depth, diffraction
 // mask), so the 32 paths a warp holds at any time mostly share the same node count and
 // node kinds — the per-path steps (q < d guards, reflection / diffraction branches, the
@@ -1979,8 +2033,14 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
       t0 = static_cast<unsigned long long>(std::chrono::duration_cast<std::chrono::nanoseconds>(
           std::chrono::system_clock::now().time_since_epoch()).count());
     }
-    if (warp)
+    if (warp) {
       kern<<<grid_n, kRefineThreads, 0, s>>>(ci, n_sub, gv, scene.view(), p.delta, p.rho, p.step_size, ro, next.get());
+      if (PCR_DEFER_VIS) {
+        PCR_LAUNCH_CHECK();
+        count_launch();
+        converged_vis_kernel<<<static_cast<unsigned>(ctx.sm_count) * 16u, 128, 0, s>>>(ci, n_sub, gv, scene.view(), ro);
+      }
+    }
     else
       kern2<<<grid_n, kRefineThreads, 0, s>>>(
           ci, n_sub, gv, scene.view(), p.delta, p.rho, p.step_size, ro, next.get(), rev_order());
