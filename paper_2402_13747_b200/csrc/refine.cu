@@ -1068,10 +1068,22 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
       // the record first; its plane (side arrays, no dependent load through the IE
       // index) only for records that survive the radius and window tests
       const double4 r4 = ldg4(nb_rec + j);
+#ifndef PCR_SCAN_EAGER
+#define PCR_SCAN_EAGER 1
+#endif
+      // PCR_SCAN_EAGER (default): the plane loads issued with the record's — one memory
+      // round trip per round instead of two dependent ones, extra bytes for rejected
+      // records. Same box: C2 refine 6.82-7.11 s -> 6.52-6.53 s, C2d3 576-592 -> 568-572
+      // ms (profiles/ab_eager_r02.log)
+      double4 pa_e, pb_e;
+      if (PCR_SCAN_EAGER) {
+        pa_e = ldg4(nb_pa + j);
+        pb_e = ldg4(nb_pb + j);
+      }
       const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r4.w));
       const uint32_t ie = static_cast<uint32_t>(w >> 33);
       const V3 sc = ld3(r4);
-      const double rad = uniform ? uradius : __ldg(&nb_pa[j].w);
+      const double rad = uniform ? uradius : PCR_SCAN_EAGER ? pa_e.w : __ldg(&nb_pa[j].w);
       const V3 pq{sl.pred[0], sl.pred[1], sl.pred[2]};
       if (norm_le(sc - pq, radius + rad)) {
         ++n_march;  // counts the reference's march_segment call
@@ -1086,8 +1098,8 @@ __device__ PCR_COOP_INLINE void coop_scan(int lane, uint32_t len, const GridView
         if (t_lo < best || (t_lo == best && lower)) {
           double bt = lower ? nextafter(best, inf) : best;
           if (__builtin_expect(((w >> 32) & 1u) != 0, 1)) {  // planar records are the common case
-            const double4 pa = ldg4(nb_pa + j);
-            const double4 pb = ldg4(nb_pb + j);
+            const double4 pa = PCR_SCAN_EAGER ? pa_e : ldg4(nb_pa + j);
+            const double4 pb = PCR_SCAN_EAGER ? pb_e : ldg4(nb_pb + j);
             if (planar_candidate_at(pv, dv, ld3(pa), ld3(pb), eps, t_lo, t_center + rad, bt, c_num, c_dn, c_t, fast))
               t = bt;
           } else {
