@@ -60,6 +60,12 @@ int pcr_create(int device, pcr_ctx** out) {
     return PCR_ERR_CUDA;
   }
   cudaDeviceGetAttribute(&ctx->c.sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (cudaHostAlloc(reinterpret_cast<void**>(&ctx->c.pin), pcr::Ctx::kPinWords * sizeof(uint64_t), cudaHostAllocDefault) !=
+      cudaSuccess) {
+    cudaStreamDestroy(ctx->c.stream);
+    delete ctx;
+    return PCR_ERR_CUDA;
+  }
   // keep freed pool memory cached across calls (stream-ordered allocator)
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -76,8 +82,10 @@ void pcr_destroy(pcr_ctx* ctx) {
   ctx->c.fan_table.release();
   ctx->c.shard.reset();      // its buffers are freed on the context's stream
   ctx->c.grid_part.reset();  // likewise the last sharded-voxelization part
+  ctx->c.trace_ws.reset();   // and the trace workspace
   cudaStreamSynchronize(ctx->c.stream);
   cudaStreamDestroy(ctx->c.stream);
+  if (ctx->c.pin) cudaFreeHost(ctx->c.pin);
   delete ctx;
 }
 

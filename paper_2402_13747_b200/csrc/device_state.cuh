@@ -145,7 +145,14 @@ struct Ctx {
   int fan_n = 0;
   DBuf<double> fan_table;  // n*6: cos phi, sin phi, sin(phi+dphi/2), cos(phi+dphi/2), sin(phi-dphi/2), cos(phi-dphi/2)
   int sm_count = 148;
+  // pinned host scratch for the per-chunk counter round trips of the trace loop: a
+  // device->host copy into pageable memory makes the driver wait for it inside
+  // cudaMemcpyAsync (measured: 0.1-1.6 s of host gaps per C2 trace stage, varying run to
+  // run); into pinned memory the copy is asynchronous and stream_wait spins on it
+  uint64_t* pin = nullptr;  // kPinWords words, [0, 8) host->device, [8, 16) device->host
+  static constexpr int kPinWords = 16;
   std::unique_ptr<GridDev> grid_part;  // the last pcr_grid_part_build's part
+  std::shared_ptr<void> trace_ws;      // trace.cu's persistent node arena / candidate / task buffers
   // work counters of the last pcr_propagate call (cone traces, visibility tests, cells, IEs)
   uint64_t last_trace[5] = {0, 0, 0, 0, 0};
   // per-kernel CUDA-event timing (pcr_set_profiling); resolved lazily

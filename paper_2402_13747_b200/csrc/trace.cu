@@ -18,6 +18,9 @@
 // key order reproduces the merged task-local + global caps. Chunks are processed
 // depth first so the frontier stays bounded.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -907,6 +910,16 @@ static void kappa_select(Ctx& ctx, const GridDev& grid, const DBuf<Cand>& cands,
 }
 
 // propagate for one TX from device initial hits; kept candidates materialised.
+struct TraceWs {
+  DBuf<Node> nodes;
+  DBuf<Cand> cands;
+  DBuf<Task> tasks;
+};
+static TraceWs& trace_ws(Ctx& ctx) {
+  if (!ctx.trace_ws) ctx.trace_ws = std::shared_ptr<void>(new TraceWs(), [](void* p) { delete static_cast<TraceWs*>(p); });
+  return *static_cast<TraceWs*>(ctx.trace_ws.get());
+}
+
 void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint32_t tx_index, const uint32_t* hit_ie,
                       const uint8_t* hit_kind, const double* hit_pos, const double* hit_nrm, const double* hit_inc,
                       uint32_t n_hits, const pcr_trace_params& p, CandDev& out, TraceStats& stats,
@@ -935,7 +948,24 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
 
   // node arena
   size_t node_cap = std::max<size_t>(1u << 20, 2ull * n_local);
-  DBuf<Node> nodes(node_cap, s);
+  // the node arena, candidate list and task buffer persist in the context across calls
+  // (TraceWs): growing them inside the chunk loop maps new pool memory now and then,
+  // measured as single 150-330 ms host stalls in a C2 trace stage of 1.3 s
+  TraceWs& ws = trace_ws(ctx);
+  struct Return {
+    TraceWs& ws;
+    DBuf<Node>& nodes;
+    DBuf<Cand>& cands;
+    DBuf<Task>& tasks;
+    ~Return() {
+      ws.nodes = std::move(nodes);
+      ws.cands = std::move(cands);
+      ws.tasks = std::move(tasks);
+    }
+  };
+  DBuf<Node> nodes = std::move(ws.nodes);
+  if (nodes.size() < node_cap) nodes.alloc(node_cap, s);
+  node_cap = nodes.size();
   DBuf<uint32_t> counters(3, s);  // n_tasks, n_nodes, n_cands
   uint32_t n_nodes = n_local;
   count_launch();
@@ -943,14 +973,19 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
                                          c, nodes.get());
   PCR_LAUNCH_CHECK();
   size_t cand_cap = 1u << 20;
-  DBuf<Cand> cands(cand_cap, s);
+  DBuf<Cand> cands = std::move(ws.cands);
+  if (cands.size() < cand_cap) cands.alloc(cand_cap, s);
+  cand_cap = cands.size();
   uint32_t n_cands = 0;
   const size_t kappa_trigger = 1u << 26;
 
   const uint32_t chunk = 1u << 18;
   DBuf<Ray> rays(chunk, s);
   size_t task_cap = 8ull * chunk;
-  DBuf<Task> tasks(task_cap, s);
+  DBuf<Task> tasks = std::move(ws.tasks);
+  if (tasks.size() < task_cap) tasks.alloc(task_cap, s);
+  task_cap = tasks.size();
+  Return give_back{ws, nodes, cands, tasks};
   DBuf<unsigned long long> alive(1, s);
   DBuf<unsigned long long> walk_stats(2, s);
   PCR_CUDA(cudaMemsetAsync(walk_stats.get(), 0, 2 * sizeof(unsigned long long), s));
@@ -981,6 +1016,15 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
   };
   push_range(0, n_local);
 
+  // development aid (PCR_TRACE_HOSTSTATS=1): host time of the chunk loop split into
+  // time blocked in stream_wait and the rest, chunk and rerun counts, to stderr
+  static const bool host_stats = std::getenv("PCR_TRACE_HOSTSTATS") != nullptr;
+  using clk = std::chrono::steady_clock;
+  double hs_wait = 0, hs_kappa = 0;
+  uint64_t hs_chunks = 0, hs_reruns = 0, hs_grow = 0;
+  const auto hs_t0 = clk::now();
+  double hs_max_pre = 0, hs_max_post = 0, hs_pre = 0, hs_post = 0;
+  auto hs_mark = clk::now();
   while (!stack.empty()) {
     StackEntry& top = stack.back();
     if (top.known && top.v_done >= top.v_total) {
@@ -1012,14 +1056,21 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
         if (nc > 0xfffffff0ull) throw Error(3, "trace: interaction arena exceeds 2^32 nodes");
         nodes.reserve(nc, n_nodes, s);
         node_cap = nc;
+        ++hs_grow;
       }
       if (n_cands + task_cap > cand_cap) {
         const size_t nc = std::max(cand_cap * 2, n_cands + task_cap);
         cands.reserve(nc, n_cands, s);
         cand_cap = nc;
       }
-      uint32_t h_cnt[3] = {0, n_nodes, n_cands};  // tasks, nodes, candidates
-      h2d(counters.get(), h_cnt, 3, s);
+      // tasks, nodes, candidates through the context's pinned scratch (see Ctx::pin)
+      uint32_t* h_in = reinterpret_cast<uint32_t*>(ctx.pin);
+      uint32_t* h_cnt = reinterpret_cast<uint32_t*>(ctx.pin + 8);
+      unsigned long long* h_out = reinterpret_cast<unsigned long long*>(ctx.pin + 10);
+      h_in[0] = 0;
+      h_in[1] = n_nodes;
+      h_in[2] = n_cands;
+      h2d(counters.get(), h_in, 3, s);
       count_launch();
       {
         KTimer kt(ctx, "cone_walk");
@@ -1037,9 +1088,22 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
       }
       PCR_LAUNCH_CHECK();
       d2h(h_cnt, counters.get(), 3, s);
-      d2h(&h_alive, alive.get(), 1, s);
-      if (!top.known) d2h(&top.v_total, top.total.get(), 1, s);
+      d2h(h_out, alive.get(), 1, s);
+      if (!top.known) d2h(reinterpret_cast<uint64_t*>(h_out + 1), top.total.get(), 1, s);
+      const auto w0 = host_stats ? clk::now() : clk::time_point{};
+      if (host_stats) {
+        const double pre = std::chrono::duration<double>(w0 - hs_mark).count();
+        hs_pre += pre;
+        hs_max_pre = std::max(hs_max_pre, pre);
+      }
       stream_wait(s);
+      if (host_stats) {
+        hs_mark = clk::now();
+        hs_wait += std::chrono::duration<double>(hs_mark - w0).count();
+        ++hs_chunks;
+      }
+      h_alive = h_out[0];
+      if (!top.known) top.v_total = h_out[1];
       top.known = true;
       n_tasks = h_cnt[0];
       if (n_tasks <= task_cap) {
@@ -1048,6 +1112,7 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
         break;
       }
       task_cap = static_cast<size_t>(n_tasks) * 5 / 4 + 1024;  // visibility did nothing: rerun the chunk
+      ++hs_reruns;
       tasks.alloc(task_cap, s);
     }
     top.v_done += was_known ? nr : std::min<uint64_t>(nr, top.v_total);
@@ -1055,6 +1120,7 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
     stats.visibility_tests += n_tasks;
     if (n_tasks == 0) continue;
     if (n_cands > kappa_trigger) {
+      const auto k0 = host_stats ? clk::now() : clk::time_point{};
       // exact pre-cap (a subset's first-kappa is a superset of its share of the global one)
       DBuf<Cand> kept;
       uint32_t nk = 0;
@@ -1062,11 +1128,24 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
       cands.reserve(std::max<size_t>(cand_cap, nk), 0, s);
       PCR_CUDA(cudaMemcpyAsync(cands.get(), kept.get(), nk * sizeof(Cand), cudaMemcpyDeviceToDevice, s));
       n_cands = nk;
+      if (host_stats) hs_kappa += std::chrono::duration<double>(clk::now() - k0).count();
     }
     // `top` may be invalidated by push_range; nothing below uses it.
     push_range(before_nodes, n_nodes - before_nodes);
+    if (host_stats) {
+      const auto now = clk::now();
+      const double post = std::chrono::duration<double>(now - hs_mark).count();
+      hs_post += post;
+      hs_max_post = std::max(hs_max_post, post);
+      hs_mark = now;
+    }
   }
 
+  if (host_stats)
+    std::fprintf(stderr, "trace loop: %.3f s, in stream_wait %.3f s, before waits %.3f s (max %.4f), after %.3f s (max %.4f), kappa pre-cap %.3f s, chunks %llu, reruns %llu, arena grows %llu\n",
+                 std::chrono::duration<double>(clk::now() - hs_t0).count(), hs_wait, hs_pre, hs_max_pre, hs_post, hs_max_post, hs_kappa,
+                 static_cast<unsigned long long>(hs_chunks), static_cast<unsigned long long>(hs_reruns),
+                 static_cast<unsigned long long>(hs_grow));
   DBuf<Cand> kept;
   uint32_t nk = 0;
   {
@@ -1102,12 +1181,12 @@ void propagate_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, uint
                                                    co);
     PCR_LAUNCH_CHECK();
   }
-  unsigned long long ws[2] = {0, 0}, unresolved = 0;
-  d2h(ws, walk_stats.get(), 2, s);
+  unsigned long long wst[2] = {0, 0}, unresolved = 0;
+  d2h(wst, walk_stats.get(), 2, s);
   PCR_CUDA(cudaMemcpyFromSymbolAsync(&unresolved, g_libm_unresolved, sizeof(unresolved), 0, cudaMemcpyDeviceToHost, s));
   stream_wait(s);
-  stats.walk_cells += ws[0];
-  stats.walk_ies += ws[1];
+  stats.walk_cells += wst[0];
+  stats.walk_ies += wst[1];
   stats.libm_unresolved += unresolved;
 }
 
