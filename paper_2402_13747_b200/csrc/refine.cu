@@ -1326,6 +1326,7 @@ __device__ __noinline__ void seed_winner(const V3& prev, const V3& dir, const V3
   const uint32_t j = j0 + win;
   const double4 r4 = ldg4(g.nb_rec + j);
   const double4 pa = ldg4(g.nb_pa + j);
+  const double4 pb = ldg4(g.nb_pb + j);
   const V3 sc = ld3(r4);
   const double rad = pa.w;
   if (!norm_le(sc - pred, 2.0 * g.sub_edge + rad)) return;
@@ -1334,7 +1335,6 @@ __device__ __noinline__ void seed_winner(const V3& prev, const V3& dir, const V3
   const uint64_t w = static_cast<uint64_t>(__double_as_longlong(r4.w));
   double bt = 1.7976931348623157e308;
   if ((w >> 32) & 1u) {
-    const double4 pb = ldg4(g.nb_pb + j);
     long long c_num = 0x7ff8dead7ff8deadll, c_dn = 0x7ff8dead7ff8deadll;
     double c_t = 0.0;
     if (!planar_candidate_at(prev, dir, ld3(pa), ld3(pb), g.hit_eps, t_lo, t_center + rad, bt, c_num, c_dn, c_t))
