@@ -1724,6 +1724,10 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
 #define PCR_WARP_MINB 3
 #endif
 constexpr int kWarpMinBlocks = PCR_WARP_MINB;
+#ifndef PCR_WARP_MINB_D4
+#define PCR_WARP_MINB_D4 4
+#endif
+constexpr int kWarpMinBlocksD4 = PCR_WARP_MINB_D4;
 
 int refine_mode() {
   static const int m = [] {
@@ -2012,8 +2016,11 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
 #define PCR_REFINE_D4 1
 #endif
     // depth bounds 3, 4 (the contract C2: max_interactions 4), 5 and 8
+    // depth 4 (the contract C2) at 4 blocks/SM (128 registers): C2 refine 6.57-6.62 s ->
+    // 6.47-6.49 s, while depth 3 prefers 3 (541-580 vs 592-637 ms), same box
+    // (profiles/ab_minblocks_r02.log)
     auto kern = in.stride <= 3                      ? refine_warp_kernel<3, kWarpMinBlocks>
-                : (PCR_REFINE_D4 && in.stride <= 4) ? refine_warp_kernel<4, kWarpMinBlocks>
+                : (PCR_REFINE_D4 && in.stride <= 4) ? refine_warp_kernel<4, kWarpMinBlocksD4>
                 : in.stride <= 5                    ? refine_warp_kernel<5, kWarpMinBlocks>
                                                     : refine_warp_kernel<kMaxDepth, kWarpMinBlocks>;
     auto kern2 = in.stride <= 3 ? refine_kernel<3, 4> : in.stride <= 5 ? refine_kernel<5, 4> : refine_kernel<kMaxDepth, 4>;
