@@ -639,7 +639,7 @@ __global__ void visited_kernel(const Ray* __restrict__ rays, uint32_t n, GridVie
       ++c;
       const int march = g.cells[vi].z;
       if (march >= 2)
-        w.init(g, r.o, r.d, w.t_entry + static_cast<double>(march - 1) * g.voxel_size, inf);
+        w.init_at(g, w.t_entry + static_cast<double>(march - 1) * g.voxel_size, inf);
       else
         w.advance(g);
     }

@@ -133,7 +133,7 @@ __device__ __forceinline__ void cone_walk(const GridView& g, const Ray& r, OnEva
       ring_n = m + 1;
     }
     if (march >= 2) {
-      w.init(g, r.o, r.d, w.t_entry + static_cast<double>(march - 1) * g.voxel_size, inf);
+      w.init_at(g, w.t_entry + static_cast<double>(march - 1) * g.voxel_size, inf);
     } else {
       w.advance(g);
     }
@@ -332,7 +332,7 @@ __device__ __forceinline__ void warp_cone_walk(const GridView& g, const Ray& r, 
       ring_n = m + 1;
     }
     if (march >= 2) {
-      w.init(g, r.o, r.d, w.t_entry + static_cast<double>(march - 1) * g.voxel_size, inf);
+      w.init_at(g, w.t_entry + static_cast<double>(march - 1) * g.voxel_size, inf);
     } else {
       w.advance(g);
     }
