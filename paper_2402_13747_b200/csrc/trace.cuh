@@ -244,6 +244,15 @@ __device__ __forceinline__ void warp_cone_walk(const GridView& g, const Ray& r, 
   const ConeConsts kc = cone_consts(half_angle, r.d);
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   const int ox = lane % 3 - 1, oy = (lane / 3) % 3 - 1, oz = lane / 9 - 1;
+  // the dedup ring is warp-uniform: one copy per warp in shared memory (broadcast reads)
+  // instead of an identical local-memory array in every lane (ncu, C2: the per-lane
+  // ring's loops were 24 % of the walk kernel's stall samples). Same box: C2 cone walk
+  // 981 -> 838 ms, C3 6.86 -> 6.13 s (profiles/ab_ring_smem_r02.log)
+#ifndef PCR_RING_SMEM
+#define PCR_RING_SMEM 1
+#endif
+  __shared__ int4 ring_s[4][8];  // walk_kernel: 128 threads = 4 warps per block
+  int4* rs = ring_s[(threadIdx.x >> 5) & 3];
   int ring[8][3];
   int ring_n = 0;
   uint32_t cells_seen = 0, ies_seen = 0;
@@ -255,8 +264,15 @@ __device__ __forceinline__ void warp_cone_walk(const GridView& g, const Ray& r, 
     if (here.x != here.y || march <= 1) {
       const int nx = w.v[0] + ox, ny = w.v[1] + oy, nz = w.v[2] + oz;
       bool valid = lane < 27 && in_bounds(g, nx, ny, nz);
-      for (int k = 0; k < ring_n && valid; ++k)
-        if (abs(nx - ring[k][0]) <= 1 && abs(ny - ring[k][1]) <= 1 && abs(nz - ring[k][2]) <= 1) valid = false;
+      if (PCR_RING_SMEM) {
+        for (int k = 0; k < ring_n && valid; ++k) {
+          const int4 e = rs[k];
+          if (abs(nx - e.x) <= 1 && abs(ny - e.y) <= 1 && abs(nz - e.z) <= 1) valid = false;
+        }
+      } else {
+        for (int k = 0; k < ring_n && valid; ++k)
+          if (abs(nx - ring[k][0]) <= 1 && abs(ny - ring[k][1]) <= 1 && abs(nz - ring[k][2]) <= 1) valid = false;
+      }
       int b = 0, cnt = 0;
       if (valid) {
         const uint32_t ni = linear_index(g, nx, ny, nz);
@@ -309,6 +325,22 @@ __device__ __forceinline__ void warp_cone_walk(const GridView& g, const Ray& r, 
         on_ie(i, pass);
       }
       // dedup ring: keep earlier evaluating voxels within Chebyshev distance 2
+      if (PCR_RING_SMEM) {
+        // lane k < ring_n tests entry k; kept entries move to their rank among the kept
+        // ones (dropping the oldest when all 8 stay), then the current voxel is appended
+        const int4 e = lane < ring_n ? rs[lane] : make_int4(0, 0, 0, 0);
+        const bool keep = lane < ring_n && abs(w.v[0] - e.x) <= 2 && abs(w.v[1] - e.y) <= 2 &&
+                          abs(w.v[2] - e.z) <= 2;
+        const uint32_t km = __ballot_sync(0xffffffffu, keep);
+        const int m = __popc(km);
+        const int drop = m == 8 ? 1 : 0;
+        const int at = __popc(km & ((1u << lane) - 1u)) - drop;
+        __syncwarp();
+        if (keep && at >= 0) rs[at] = e;
+        if (lane == 0) rs[m - drop] = make_int4(w.v[0], w.v[1], w.v[2], 0);
+        ring_n = m - drop + 1;
+        __syncwarp();
+      } else {
       int m = 0;
       for (int k = 0; k < ring_n; ++k) {
         if (abs(w.v[0] - ring[k][0]) <= 2 && abs(w.v[1] - ring[k][1]) <= 2 && abs(w.v[2] - ring[k][2]) <= 2) {
@@ -330,6 +362,7 @@ __device__ __forceinline__ void warp_cone_walk(const GridView& g, const Ray& r, 
       ring[m][1] = w.v[1];
       ring[m][2] = w.v[2];
       ring_n = m + 1;
+      }
     }
     if (march >= 2) {
       w.init_at(g, w.t_entry + static_cast<double>(march - 1) * g.voxel_size, inf);
