@@ -256,8 +256,17 @@ __device__ __forceinline__ void warp_cone_walk(const GridView& g, const Ray& r, 
   int ring[8][3];
   int ring_n = 0;
   uint32_t cells_seen = 0, ies_seen = 0;
-  Walker w;
-  w.init(g, r.o, r.d, 0.0, inf);
+  // the walker is warp-uniform too: one copy per warp in shared memory, stepped by
+  // lane 0 between two __syncwarp()s, read by every lane (C2 cone walk 845 -> 747 ms,
+  // C3 6.17 -> 5.81 s same box, profiles/ab_walker_smem_r02.log)
+#ifndef PCR_WALKER_SMEM
+#define PCR_WALKER_SMEM 1
+#endif
+  __shared__ Walker walk_s[4];
+  Walker w_local;
+  Walker& w = PCR_WALKER_SMEM ? walk_s[(threadIdx.x >> 5) & 3] : w_local;
+  if (!PCR_WALKER_SMEM || lane == 0) w.init(g, r.o, r.d, 0.0, inf);
+  __syncwarp();
   while (w.active) {
     const int4 here = g.cells[linear_index(g, w.v[0], w.v[1], w.v[2])];
     const int march = here.z;
@@ -364,11 +373,15 @@ __device__ __forceinline__ void warp_cone_walk(const GridView& g, const Ray& r, 
       ring_n = m + 1;
       }
     }
-    if (march >= 2) {
-      w.init_at(g, w.t_entry + static_cast<double>(march - 1) * g.voxel_size, inf);
-    } else {
-      w.advance(g);
+    __syncwarp();
+    if (!PCR_WALKER_SMEM || lane == 0) {
+      if (march >= 2) {
+        w.init_at(g, w.t_entry + static_cast<double>(march - 1) * g.voxel_size, inf);
+      } else {
+        w.advance(g);
+      }
     }
+    __syncwarp();
   }
   if (n_cells) *n_cells += cells_seen;
   if (n_ies) *n_ies += ies_seen;
