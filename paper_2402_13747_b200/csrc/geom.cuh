@@ -587,21 +587,42 @@ __device__ inline bool warp_segment_visible(const V3& origin, const V3& target, 
   if (span <= 1e-9) return true;
   const V3 o2 = origin + er * d;
   const double cell_reach = g.voxel_radius + g.sub_radius;
-  Walker w;
-  w.init(g, origin, d, 0.0, dist);
+  // the walker is warp-uniform: one copy per warp in shared memory, stepped by lane 0
+  // between two __syncwarp()s (as in warp_cone_walk); callers run 128-thread blocks.
+  // Same box: C3 visibility 11.34 -> 9.74 s, C2 297 -> 264 ms
+  // (profiles/ab_segvis_walker_smem_r02.log)
+#ifndef PCR_SEGVIS_WALKER_SMEM
+#define PCR_SEGVIS_WALKER_SMEM 1
+#endif
+  __shared__ Walker segvis_walk_s[4];
+  Walker w_local;
+  Walker& w = PCR_SEGVIS_WALKER_SMEM ? segvis_walk_s[(threadIdx.x >> 5) & 3] : w_local;
+  __syncwarp();  // every lane is past the previous call's last read of the shared walker
+  if (!PCR_SEGVIS_WALKER_SMEM || lane == 0) w.init(g, origin, d, 0.0, dist);
+  __syncwarp();
+  auto advance = [&]() {
+    if (!PCR_SEGVIS_WALKER_SMEM) return w.advance(g);
+    int a = 0;
+    if (lane == 0) a = w.advance(g);
+    a = __shfl_sync(0xffffffffu, a, 0);
+    __syncwarp();
+    return a;
+  };
   int axis = -1;
   int skip = 0;
   while (w.active) {
     // empty-space skipping, as in segment_visible (warp-uniform)
     if (skip > 0) {
       --skip;
-      axis = w.advance(g);
+      __syncwarp();
+      axis = advance();
       continue;
     }
     const int m = g.march_ok ? g.cells[linear_index(g, w.v[0], w.v[1], w.v[2])].z : 0;
     if (m >= 2) {
       skip = m - 2;
-      axis = w.advance(g);
+      __syncwarp();
+      axis = advance();
       continue;
     }
     int off[3];
@@ -667,7 +688,8 @@ __device__ inline bool warp_segment_visible(const V3& origin, const V3& target, 
       }
       if (__any_sync(0xffffffffu, blocked)) return false;
     }
-    axis = w.advance(g);
+    __syncwarp();
+      axis = advance();
   }
   return true;
 }
