@@ -625,21 +625,24 @@ __device__ inline bool warp_segment_visible(const V3& origin, const V3& target, 
       axis = advance();
       continue;
     }
-    int off[3];
+    // this lane's cell offset: the 27-neighbourhood, or the far slab across the stepped
+    // axis (selects instead of an array indexed by the axis, which lived in local memory)
+    int ox_, oy_, oz_;
     bool mine;
     if (axis < 0) {
       mine = lane < 27;
-      off[0] = lane % 3 - 1;
-      off[1] = (lane / 3) % 3 - 1;
-      off[2] = lane / 9 - 1;
+      ox_ = lane % 3 - 1;
+      oy_ = (lane / 3) % 3 - 1;
+      oz_ = lane / 9 - 1;
     } else {
       mine = lane < 9;
       const int u = lane % 3 - 1, v = (lane / 3) % 3 - 1;
-      off[axis] = w.step[axis];
-      off[(axis + 1) % 3] = u;
-      off[(axis + 2) % 3] = v;
+      const int st = w.step[axis];
+      ox_ = axis == 0 ? st : axis == 1 ? v : u;
+      oy_ = axis == 1 ? st : axis == 2 ? v : u;
+      oz_ = axis == 2 ? st : axis == 0 ? v : u;
     }
-    const int nx = w.v[0] + off[0], ny = w.v[1] + off[1], nz = w.v[2] + off[2];
+    const int nx = w.v[0] + ox_, ny = w.v[1] + oy_, nz = w.v[2] + oz_;
     int b = 0, cnt = 0;
     if (mine && in_bounds(g, nx, ny, nz)) {
       const int4 cell = g.cells[linear_index(g, nx, ny, nz)];
