@@ -411,13 +411,23 @@ __device__ __forceinline__ uint64_t state_hash(const RNode* nd, int d) {
   }
   return h;
 }
+// A second saved hash refreshed every PCR_CYC_FIXED iterations catches short cycles that
+// start late (after Brent's last power-of-two save). Measured on C2: 2.006 G -> 1.985 G
+// iterations (same outcomes and hash), refine 6.48 -> 6.44 s; so the ~685 k paths that
+// run to rho are not short-periodic — they drift (profiles/ab_cycle_fixed_r02.log)
+#ifndef PCR_CYC_FIXED
+#define PCR_CYC_FIXED 64
+#endif
 template <int D>
 struct CycleCheck {
   uint64_t h1, h2, hs;   // hashes of S_{i-1}, S_{i-2} and of Brent's saved state
   int saved_iter, power, lam, pend_at;
+  uint64_t hf;           // PCR_CYC_FIXED > 0: a second saved hash, refreshed every PCR_CYC_FIXED iterations
+  int fixed_iter;
   Snapshot<D> pending;   // a state suspected to recur at iteration pend_at
   __device__ __forceinline__ void init(const RNode* nd, int d) {
-    h1 = h2 = hs = state_hash<D>(nd, d);
+    h1 = h2 = hs = hf = state_hash<D>(nd, d);
+    fixed_iter = -1;
     saved_iter = -1;
     power = 1;
     lam = 0;
@@ -432,7 +442,8 @@ struct CycleCheck {
       pend_at = -1;
     }
     if (!cyc && pend_at < 0) {
-      const int p = h == h1 ? 1 : h == h2 ? 2 : h == hs ? i - saved_iter : 0;
+      int p = h == h1 ? 1 : h == h2 ? 2 : h == hs ? i - saved_iter : 0;
+      if (PCR_CYC_FIXED > 0 && p == 0 && h == hf) p = i - fixed_iter;
       if (p > 0) {
         take_snapshot(pending, nd, d);
         pend_at = i + p;
@@ -445,6 +456,10 @@ struct CycleCheck {
       saved_iter = i;
       power <<= 1;
       lam = 0;
+    }
+    if (PCR_CYC_FIXED > 0 && (i + 1) % (PCR_CYC_FIXED > 0 ? PCR_CYC_FIXED : 1) == 0) {
+      hf = h;
+      fixed_iter = i;
     }
     return cyc;
   }
