@@ -596,6 +596,7 @@ __device__ inline bool warp_segment_visible(const V3& origin, const V3& target, 
 #endif
   __shared__ Walker segvis_walk_s[4];
   Walker w_local;
+  if (PCR_SEGVIS_WALKER_SMEM && blockDim.x > 128) __trap();  // one shared walker per warp of a 128-thread block
   Walker& w = PCR_SEGVIS_WALKER_SMEM ? segvis_walk_s[(threadIdx.x >> 5) & 3] : w_local;
   __syncwarp();  // every lane is past the previous call's last read of the shared walker
   if (!PCR_SEGVIS_WALKER_SMEM || lane == 0) w.init(g, origin, d, 0.0, dist);

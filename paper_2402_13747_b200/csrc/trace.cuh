@@ -264,6 +264,7 @@ __device__ __forceinline__ void warp_cone_walk(const GridView& g, const Ray& r, 
 #endif
   __shared__ Walker walk_s[4];
   Walker w_local;
+  if ((PCR_WALKER_SMEM || PCR_RING_SMEM) && blockDim.x > 128) __trap();  // per-warp shared state of a 128-thread block
   Walker& w = PCR_WALKER_SMEM ? walk_s[(threadIdx.x >> 5) & 3] : w_local;
   __syncwarp();  // every lane is past the previous walk's last read of the shared walker
   if (!PCR_WALKER_SMEM || lane == 0) w.init(g, r.o, r.d, 0.0, inf);
