@@ -465,6 +465,81 @@ struct Walker {
     active = true;
   }
 
+  // init() for a walker in shared memory, computed by the warp: lanes 0..2 take one axis
+  // each (box clip, step, increment, entry voxel, first crossing), the entry point is
+  // reduced over the axes in the serial order on every lane, and each lane writes its
+  // axis (lane 0 the rest). Called by all 32 lanes; same fields, same bits as init().
+  __device__ __forceinline__ void init_warp(const GridView& g, const V3& origin, const V3& dir, double t0,
+                                            double t1, int lane) {
+    const int a = lane < 3 ? lane : 0;
+    const double od = a == 0 ? origin.x : a == 1 ? origin.y : origin.z;
+    const double dd = a == 0 ? dir.x : a == 1 ? dir.y : dir.z;
+    const double gd = a == 0 ? g.origin.x : a == 1 ? g.origin.y : g.origin.z;
+    const double bmin = gd;
+    const double bmax = gd + static_cast<double>(g.dims[a]) * g.voxel_size;
+    const bool pa = fabs(dd) < kTiny;
+    const bool out = pa && (od < bmin || od > bmax);
+    double lo_a = 0.0, hi_a = 0.0;
+    if (!pa) {
+      lo_a = (bmin - od) / dd;
+      hi_a = (bmax - od) / dd;
+      if (lo_a > hi_a) {
+        const double tmp = lo_a;
+        lo_a = hi_a;
+        hi_a = tmp;
+      }
+    }
+    double lo = t0, hi = t1;
+    bool any_out = false;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const bool pb = __shfl_sync(0xffffffffu, pa, b);
+      const bool ob = __shfl_sync(0xffffffffu, out, b);
+      const double tab = __shfl_sync(0xffffffffu, lo_a, b), tbb = __shfl_sync(0xffffffffu, hi_a, b);
+      any_out = any_out || ob;
+      if (!pb) {
+        lo = smax(lo, tab);
+        hi = smin(hi, tbb);
+      }
+    }
+    const bool ok = !any_out && !(lo > hi);
+    if (lane < 3) {
+      ta[a] = lo_a;
+      tb[a] = hi_a;
+      par[a] = pa;
+      int st = 0;
+      double de = 0.0;
+      if (dd > kTiny) {
+        st = 1;
+        de = g.voxel_size / dd;
+      } else if (dd < -kTiny) {
+        st = -1;
+        de = -g.voxel_size / dd;
+      }
+      step[a] = st;
+      delta[a] = de;
+      if (ok) {
+        const double pnt = od + lo * dd;
+        const int va = sclamp(static_cast<int>(floor((pnt - gd) / g.voxel_size)), 0, g.dims[a] - 1);
+        v[a] = va;
+        if (st > 0)
+          t_next[a] = ((gd + static_cast<double>(va + 1) * g.voxel_size) - od) / dd;
+        else if (st < 0)
+          t_next[a] = ((gd + static_cast<double>(va) * g.voxel_size) - od) / dd;
+        else
+          t_next[a] = __longlong_as_double(0x7ff0000000000000ll);
+      }
+    }
+    if (lane == 0) {
+      o = origin;
+      d = dir;
+      t_end = t1;
+      miss = any_out;
+      if (ok) t_entry = lo;
+      active = ok;
+    }
+  }
+
   // Returns the stepped axis, or -1 when the walk ended.
   __device__ __forceinline__ int advance(const GridView& g) {
     if (!active) return -1;
@@ -599,7 +674,13 @@ __device__ inline bool warp_segment_visible(const V3& origin, const V3& target, 
   if (PCR_SEGVIS_WALKER_SMEM && blockDim.x > 128) __trap();  // one shared walker per warp of a 128-thread block
   Walker& w = PCR_SEGVIS_WALKER_SMEM ? segvis_walk_s[(threadIdx.x >> 5) & 3] : w_local;
   __syncwarp();  // every lane is past the previous call's last read of the shared walker
-  if (!PCR_SEGVIS_WALKER_SMEM || lane == 0) w.init(g, origin, d, 0.0, dist);
+#ifndef PCR_SEGVIS_WARP_INIT
+#define PCR_SEGVIS_WARP_INIT 1
+#endif
+  if (PCR_SEGVIS_WALKER_SMEM && PCR_SEGVIS_WARP_INIT)
+    w.init_warp(g, origin, d, 0.0, dist, lane);
+  else if (!PCR_SEGVIS_WALKER_SMEM || lane == 0)
+    w.init(g, origin, d, 0.0, dist);
   __syncwarp();
   auto advance = [&]() {
     if (!PCR_SEGVIS_WALKER_SMEM) return w.advance(g);
