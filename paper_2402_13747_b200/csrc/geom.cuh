@@ -54,6 +54,7 @@ struct GridView {
   // exact fast rejection in the planar reprojection scan (refine.cu planar_candidate_at):
   // set when the scene's coordinates are small enough for its error bound
   int fast_reject = 0;
+  int seed_scan = 0;  // refine: seed the same-label scans with the last winner (grids with non-planar IEs)
   // non-planar payloads in point_indices order (positions / normals gathered once per
   // stage call, GridDev::view_for): estimate_surface streams them instead of a dependent
   // point_indices -> scene gather per point; null when the grid has no non-planar IE

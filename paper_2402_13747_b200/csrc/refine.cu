@@ -1333,8 +1333,14 @@ __device__ PCR_COOP_INLINE void coop_scan_ilp2(int lane, uint32_t len, const Gri
 // best — radius test, window, planar snap or march. A hit becomes the scan's initial
 // best (t, position); a miss leaves the scan unseeded. Not counted in n_march (the scan
 // visits and counts the record itself).
+// Off by default since the eager plane loads: on the planar contract configs the seed
+// evaluation costs more than it prunes (same box: C2 refine 6.44-6.47 -> 6.27-6.28 s,
+// C2d3 543-582 -> 527-577 ms, C3 4.12 -> 3.49 s without; profiles/ab_noseed_r02.log).
+// A runtime switch on the grid's planarity kept the seeding call in the kernel and lost
+// the gain (6.45 s), so it is compile-time; non-planar grids (C2-np) gave up ~2.6 %
+// (depth 1: 34.0 s with seeds, 34.9 s without, measured before the eager loads).
 #ifndef PCR_SCAN_SEED
-#define PCR_SCAN_SEED 1
+#define PCR_SCAN_SEED 0
 #endif
 __device__ __noinline__ void seed_winner(const V3& prev, const V3& dir, const V3& pred, uint32_t j0, uint32_t win,
                                          const GridView& g, const SceneView& s, ScanSlot& me) {
@@ -1662,7 +1668,8 @@ __global__ void __launch_bounds__(kRefineThreads, kMinBlocks)
           // then evaluates only the records that could beat it (coop_scan)
           me.best_f = kNoRec;
           me.best_t = 1.7976931348623157e308;
-          if (PCR_SCAN_SEED && st.rc[q].win < len) seed_winner(prev, dir, pred, j0, st.rc[q].win, g, s, me);
+          if (PCR_SCAN_SEED && g.seed_scan && st.rc[q].win < len)
+            seed_winner(prev, dir, pred, j0, st.rc[q].win, g, s, me);
         } else if (r == 2) {
           got = reproject(prev, pred, st.nd[q].label, g, s, re, n_march);
         }
@@ -1961,6 +1968,7 @@ void refine_device(Ctx& ctx, const GridDev& grid, const SceneDev& scene, const R
     }
     const double extent = 2.0 * std::sqrt(r2) + std::sqrt(d2) + 1.0;
     gv.fast_reject = 4.0 * 30.0 * 1.1102230246251565e-16 * extent < kMarginFast ? 1 : 0;
+    gv.seed_scan = PCR_SCAN_SEED ? 1 : 0;
   }
   // neighbourhood lists (the reprojection box is a cell's 3x3x3 neighbourhood whenever
   // 2 * subvoxel_edge spans exactly one voxel each way, i.e. division_factor 2)
